@@ -1,0 +1,273 @@
+// fp64 complex FFT building blocks for sm_100a.
+//
+// One transform of length M (power of two, 1..4096) is owned by T = M/E
+// threads, each holding E = min(16, M) complex values in registers.  The
+// transform is a Stockham auto-sort DIT with radix plan [b, 16, 16, ...]
+// (b = M / 16^a in {1,2,4,8}); every exchange between stages goes through a
+// padded shared-memory buffer (one pad slot per 16 elements keeps the
+// 16-byte accesses conflict-free).  Layout contract, identical on entry and
+// exit: register r of thread t holds element / frequency  t + T*r.
+//
+// Twiddles come from one table W_4096^m (m < 4096) in global memory (L1
+// resident); W_M^m = W_4096^(m * 4096/M).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ttagg {
+
+struct cplx {
+  double x, y;
+};
+
+__device__ __forceinline__ cplx mk(double x, double y) { return cplx{x, y}; }
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cplx{a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return cplx{a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cplx{fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
+}
+__device__ __forceinline__ cplx cmulc(cplx a, cplx b) {  // a * conj(b)
+  return cplx{fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y)};
+}
+__device__ __forceinline__ cplx cconj(cplx a) { return cplx{a.x, -a.y}; }
+__device__ __forceinline__ cplx cscale(cplx a, double s) { return cplx{a.x * s, a.y * s}; }
+__device__ __forceinline__ cplx mul_mi(cplx a) { return cplx{a.y, -a.x}; }  // * (-i)
+__device__ __forceinline__ cplx mul_pi(cplx a) { return cplx{-a.y, a.x}; }  // * (+i)
+
+__device__ __forceinline__ cplx ld_c(const double2* p) {
+  double2 v = __ldg(p);
+  return cplx{v.x, v.y};
+}
+__device__ __forceinline__ cplx lds_c(const double2* p) {
+  double2 v = *p;
+  return cplx{v.x, v.y};
+}
+__device__ __forceinline__ void sts_c(double2* p, cplx v) { *p = make_double2(v.x, v.y); }
+
+// ---------------------------------------------------------------------------
+// small DFTs (forward, W = exp(-2 pi i / R)), in place on v[0..R)
+// ---------------------------------------------------------------------------
+template <int R>
+struct DFT;
+
+template <>
+struct DFT<1> {
+  __device__ __forceinline__ static void run(cplx*) {}
+};
+
+template <>
+struct DFT<2> {
+  __device__ __forceinline__ static void run(cplx* v) {
+    cplx a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+
+__device__ __forceinline__ void dft4(cplx& a0, cplx& a1, cplx& a2, cplx& a3) {
+  cplx s02 = cadd(a0, a2), d02 = csub(a0, a2);
+  cplx s13 = cadd(a1, a3), d13 = mul_mi(csub(a1, a3));
+  a0 = cadd(s02, s13);
+  a2 = csub(s02, s13);
+  a1 = cadd(d02, d13);
+  a3 = csub(d02, d13);
+}
+
+template <>
+struct DFT<4> {
+  __device__ __forceinline__ static void run(cplx* v) { dft4(v[0], v[1], v[2], v[3]); }
+};
+
+#define TTAGG_SQRT1_2 0.70710678118654752440
+#define TTAGG_COS_PI8 0.92387953251128675613
+#define TTAGG_SIN_PI8 0.38268343236508977173
+
+// multiply by W_16^m, m compile-time in [0, 16)
+template <int m>
+__device__ __forceinline__ cplx w16(cplx a) {
+  constexpr int k = m & 15;
+  if constexpr (k == 0) return a;
+  else if constexpr (k == 4) return mul_mi(a);
+  else if constexpr (k == 8) return cplx{-a.x, -a.y};
+  else if constexpr (k == 12) return mul_pi(a);
+  else if constexpr (k == 2) return cplx{TTAGG_SQRT1_2 * (a.x + a.y), TTAGG_SQRT1_2 * (a.y - a.x)};
+  else if constexpr (k == 6) return cplx{TTAGG_SQRT1_2 * (a.y - a.x), -TTAGG_SQRT1_2 * (a.x + a.y)};
+  else if constexpr (k == 10) return cplx{-TTAGG_SQRT1_2 * (a.x + a.y), TTAGG_SQRT1_2 * (a.x - a.y)};
+  else if constexpr (k == 14) return cplx{TTAGG_SQRT1_2 * (a.x - a.y), TTAGG_SQRT1_2 * (a.x + a.y)};
+  else {
+    // general: cos(2 pi k/16) - i sin(2 pi k/16)
+    constexpr double c[16] = {1.0, TTAGG_COS_PI8, TTAGG_SQRT1_2, TTAGG_SIN_PI8, 0.0, -TTAGG_SIN_PI8,
+                              -TTAGG_SQRT1_2, -TTAGG_COS_PI8, -1.0, -TTAGG_COS_PI8, -TTAGG_SQRT1_2,
+                              -TTAGG_SIN_PI8, 0.0, TTAGG_SIN_PI8, TTAGG_SQRT1_2, TTAGG_COS_PI8};
+    constexpr double wr = c[k];
+    constexpr double wi = -c[(k + 12) & 15];  // -sin(2 pi k / 16) = -cos(2 pi (k - 4)/16)
+    return cplx{fma(a.x, wr, -a.y * wi), fma(a.x, wi, a.y * wr)};
+  }
+}
+
+template <>
+struct DFT<8> {
+  __device__ __forceinline__ static void run(cplx* v) {
+    // split n = 2 n1 + n2: DFT4 over evens and odds, then W_8 twiddles
+    cplx e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    cplx o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4(e0, e1, e2, e3);
+    dft4(o0, o1, o2, o3);
+    o1 = w16<2>(o1);
+    o2 = w16<4>(o2);
+    o3 = w16<6>(o3);
+    v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
+    v[1] = cadd(e1, o1); v[5] = csub(e1, o1);
+    v[2] = cadd(e2, o2); v[6] = csub(e2, o2);
+    v[3] = cadd(e3, o3); v[7] = csub(e3, o3);
+  }
+};
+
+template <>
+struct DFT<16> {
+  __device__ __forceinline__ static void run(cplx* v) {
+    // n = 4 n1 + n2 ; k = k1 + 4 k2
+    // step 1: for each n2, DFT4 over n1 of v[4 n1 + n2]
+    dft4(v[0], v[4], v[8], v[12]);
+    dft4(v[1], v[5], v[9], v[13]);
+    dft4(v[2], v[6], v[10], v[14]);
+    dft4(v[3], v[7], v[11], v[15]);
+    // now v[4 k1 + n2] = B[n2][k1]; twiddle W16^(n2 k1)
+    v[5] = w16<1>(v[5]);
+    v[6] = w16<2>(v[6]);
+    v[7] = w16<3>(v[7]);
+    v[9] = w16<2>(v[9]);
+    v[10] = w16<4>(v[10]);
+    v[11] = w16<6>(v[11]);
+    v[13] = w16<3>(v[13]);
+    v[14] = w16<6>(v[14]);
+    v[15] = w16<9>(v[15]);
+    // step 3: for each k1, DFT4 over n2 of B[n2][k1] = v[4 k1 + n2] -> X[k1 + 4 k2]
+    dft4(v[0], v[1], v[2], v[3]);
+    dft4(v[4], v[5], v[6], v[7]);
+    dft4(v[8], v[9], v[10], v[11]);
+    dft4(v[12], v[13], v[14], v[15]);
+    // v[4 k1 + k2] = X[k1 + 4 k2]: transpose 4x4 to natural order
+    cplx t;
+    t = v[1]; v[1] = v[4]; v[4] = t;
+    t = v[2]; v[2] = v[8]; v[8] = t;
+    t = v[3]; v[3] = v[12]; v[12] = t;
+    t = v[6]; v[6] = v[9]; v[9] = t;
+    t = v[7]; v[7] = v[13]; v[13] = t;
+    t = v[11]; v[11] = v[14]; v[14] = t;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Stockham transform of length M
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+__host__ __device__ constexpr int fft_e(int M) { return M >= 16 ? 16 : M; }
+__host__ __device__ constexpr int fft_t(int M) { return M / fft_e(M); }
+// first-stage radix b = M / 16^a
+__host__ __device__ constexpr int fft_first_radix(int M) {
+  return M >= 16 ? (1 << (ilog2c(M) % 4)) : M;
+}
+__host__ __device__ constexpr int fft_smem_elems(int M) { return M + (M >> 4) + 1; }
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+constexpr int TW_BASE = 4096;  // twiddle table W_4096^m
+
+// One stage.  Registers: element t + T*r in v[r] on entry (read pattern).
+template <int M, int R, int NS, bool LAST>
+__device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw) {
+  constexpr int E = fft_e(M);
+  constexpr int T = fft_t(M);
+  constexpr int G = E / R;  // butterflies per thread
+#pragma unroll
+  for (int u = 0; u < G; ++u) {
+    const int q = t + T * u;
+    cplx x[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) x[i] = v[u + i * G];
+    if constexpr (NS > 1) {
+      const int qm = q & (NS - 1);
+#pragma unroll
+      for (int i = 1; i < R; ++i) {
+        // W_{NS R}^{i qm} = W_4096^{i qm 4096/(NS R)}
+        const int idx = (i * qm) * (TW_BASE / (NS * R));
+        x[i] = cmul(x[i], ld_c(tw + idx));
+      }
+    }
+    DFT<R>::run(x);
+    if constexpr (LAST) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[u + i * G] = x[i];
+    } else {
+      const int base = (q / NS) * NS * R + (q & (NS - 1));
+#pragma unroll
+      for (int i = 0; i < R; ++i) sts_c(sm + pad16(base + i * NS), x[i]);
+    }
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void fft_load_regs(cplx (&v)[fft_e(M)], int t, const double2* sm) {
+  constexpr int E = fft_e(M);
+  constexpr int T = fft_t(M);
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r] = lds_c(sm + pad16(t + T * r));
+}
+
+// Forward FFT of length M (no normalisation).  All threads of the CTA must
+// call it (it contains __syncthreads when M > 16); `sm` is this transform's
+// private buffer of fft_smem_elems(M) slots.
+template <int M>
+__device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw) {
+  if constexpr (M <= 16) {
+    DFT<M>::run(v);
+    // DFT<R> leaves natural order, and with T == 1 register r == frequency r
+  } else {
+    constexpr int b = fft_first_radix(M);
+    constexpr int a = (ilog2c(M) - ilog2c(b)) / 4;  // number of radix-16 stages
+    static_assert(a >= 1, "M >= 16");
+    int ns_done;
+    if constexpr (b > 1) {
+      fft_stage<M, b, 1, false>(v, t, sm, tw);
+      __syncthreads();
+      fft_load_regs<M>(v, t, sm);
+      __syncthreads();
+    }
+    constexpr int NS1 = b;
+    // radix-16 stages: NS = b, 16 b, 256 b, ...
+    if constexpr (a == 1) {
+      fft_stage<M, 16, NS1, true>(v, t, sm, tw);
+    } else if constexpr (a == 2) {
+      fft_stage<M, 16, NS1, false>(v, t, sm, tw);
+      __syncthreads();
+      fft_load_regs<M>(v, t, sm);
+      __syncthreads();
+      fft_stage<M, 16, NS1 * 16, true>(v, t, sm, tw);
+    } else {
+      static_assert(a == 3, "M <= 4096");
+      fft_stage<M, 16, NS1, false>(v, t, sm, tw);
+      __syncthreads();
+      fft_load_regs<M>(v, t, sm);
+      __syncthreads();
+      fft_stage<M, 16, NS1 * 16, false>(v, t, sm, tw);
+      __syncthreads();
+      fft_load_regs<M>(v, t, sm);
+      __syncthreads();
+      fft_stage<M, 16, NS1 * 256, true>(v, t, sm, tw);
+    }
+    (void)ns_done;
+  }
+}
+
+// Inverse (unnormalised) via conj(FFT(conj(x))).
+template <int M>
+__device__ __forceinline__ void fft_inv(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw) {
+  constexpr int E = fft_e(M);
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r].y = -v[r].y;
+  fft_fwd<M>(v, t, sm, tw);
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r].y = -v[r].y;
+}
+
+}  // namespace ttagg

@@ -1,0 +1,1718 @@
+// B200-native RHS evaluator for the multi-particle Smoluchowski equations.
+//
+// Gain P^(d) (rhs.py:234-302 TT, rhs.py:345-391 CP) is an fp64 FFT
+// convolution of length L = d*Np (alias-free since L >= d*N - d + 1, SURVEY
+// §7), evaluated as a four-step transform L = (d*N1) x N2 over the size
+// index viewed as o = n1*N2 + n2:
+//
+//   pass A  (per column pair, per n2): the column transform over n1 — a
+//           length-d*N1 DFT with only N1 nonzero inputs, done as d twisted
+//           length-N1 FFTs ("residues"); two real columns ride in one
+//           complex FFT and are separated through the Hermitian mirror;
+//           only a half set of rows is kept; rows are twiddled by
+//           W_L^(n2*kappa) and written to the exchange buffer T.  The
+//           column sums needed by the loss (<F[:,r], n>) fall out of the
+//           same read.
+//   pass B  (per block of 8 rows kappa, streaming over all columns): the
+//           length-N2 row FFTs, then the per-frequency product over modes
+//           and sum over ranks (CP) or the spectral matrix chain (TT); then
+//           the (d-1)-position shift, the inverse row FFT and the inverse
+//           twiddle, written to U.
+//   pass C  (per n2): the inverse column transform, pruned to the N1
+//           outputs that land on sizes 1..N, scaled by 1/(L d!).
+//
+// Loss Q^(d) (rhs.py:305-338, 394-414): qcoef reduces the pass-A column
+// sums to the per-rank scalars (CP) / contracted chain (TT); the combine
+// kernel applies the tail GEMV, adds all orders and writes p, q, s (or the
+// fused RK2 stage update, integrator.py:153-157).
+//
+// Data layout in HBM: every length-N vector of the hot loop lives in the
+// "perm" layout (element o = n1*N2 + n2 at n2*N1 + n1), so pass A reads each
+// column with unit stride; factor columns / TT fibers are stored once, at
+// upload, in that layout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fft.cuh"
+#include "ttagg_b200.h"
+
+using namespace ttagg;
+
+namespace {
+
+constexpr int MAXD = 8;
+constexpr int MAXRES = MAXD / 2 + 1;
+constexpr int MAXORD = 8;
+constexpr int LSPLIT = 11;
+constexpr int LLO = 1 << LSPLIT;
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(TTAGG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TRY(x)            \
+  do {                    \
+    int rc_ = (x);        \
+    if (rc_) return rc_;  \
+  } while (0)
+
+struct Geom {
+  int64_t N = 0, Np = 0;
+  int N1 = 0, N2 = 0;
+};
+
+int64_t next_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int make_geom(int64_t N, Geom* g) {
+  if (N < 2) return fail(TTAGG_ERR_ARG, "concentration state must be a vector of length >= 2");
+  int64_t Np = std::max<int64_t>(64, next_pow2(N));
+  int64_t N1 = std::max<int64_t>(4, Np / 256);
+  if (N1 > 4096)
+    return fail(TTAGG_ERR_UNSUPPORTED, "N = " + std::to_string(N) + " exceeds the supported 2^20 size classes");
+  g->N = N;
+  g->Np = Np;
+  g->N1 = (int)N1;
+  g->N2 = (int)(Np / N1);
+  return TTAGG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// per-order transform plan (tables live in device memory)
+// ---------------------------------------------------------------------------
+struct OrderPlan {
+  int d = 0;
+  Geom g;
+  int64_t L = 0;  // d * Np
+  int K = 0;      // d * N1
+  int nres = 0;
+  int res_base[MAXRES] = {0};
+  int res_cnt[MAXRES] = {0};
+  int K_rows = 0;
+  double2* tabK = nullptr;    // W_K^m, m < K
+  double2* tabLlo = nullptr;  // W_L^m, m < 2048
+  double2* tabLhi = nullptr;  // W_L^(m*2048), m < ceil(L/2048)
+  int* rowkappa = nullptr;    // kappa of every exchange row (-1: pad)
+};
+
+void host_twiddles(std::vector<double2>& out, int64_t L, int64_t count, int64_t stride) {
+  // W_L^(m*stride) = exp(-2 pi i m stride / L), long double then rounded
+  out.resize(count);
+  const long double twopi = 6.283185307179586476925286766559005768L;
+  for (int64_t m = 0; m < count; ++m) {
+    int64_t e = (m * stride) % L;
+    long double ang = twopi * (long double)e / (long double)L;
+    out[m] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+  }
+}
+
+}  // namespace
+
+struct ttagg_ctx {
+  int device = 0;
+  std::mutex mu;
+  double2* tw4096 = nullptr;
+  std::map<std::pair<int, int64_t>, OrderPlan*> plans;
+  // workspaces
+  double2* T = nullptr;
+  size_t T_bytes = 0;
+  double2* U = nullptr;
+  size_t U_bytes = 0;
+  double* pbuf = nullptr;
+  size_t pbuf_bytes = 0;
+  double2* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  double* vec = nullptr;  // general vectors (natural/perm state, outputs)
+  size_t vec_bytes = 0;
+  double* diagp = nullptr;  // per-block diag partials
+  size_t diagp_bytes = 0;
+  double* diag = nullptr;  // 2 x 8 finalized diag
+  int64_t* book = nullptr; // device step bookkeeping
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  double prof_acc[5] = {0, 0, 0, 0, 0};
+};
+
+struct ttagg_kernel {
+  ttagg_ctx* ctx = nullptr;
+  int kind = 0, d = 0;
+  int64_t N = 0;
+  Geom g;
+  int C = 0, C_pad = 0;
+  double* X = nullptr;  // [C_pad][Np]
+  int R = 0;            // CP: local ranks
+  int ranks[MAXD + 1] = {0};
+  int core_off[MAXD + 1] = {0};
+  int Rmax = 0;
+  int ntail = 0;
+  int* tail_cols = nullptr;
+  int nblk = 0;  // pass-A blocks per column (dot partials)
+  double* dots = nullptr;
+  double* coef = nullptr;
+  OrderPlan* plan = nullptr;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ cplx twL(const double2* __restrict__ lo, const double2* __restrict__ hi, long long m) {
+  return cmul(ld_c(hi + (m >> LSPLIT)), ld_c(lo + (m & (LLO - 1))));
+}
+
+// state value at perm index e: n + alpha*k rounded as numpy does (no fma)
+__device__ __forceinline__ double state_at(const double* __restrict__ nv, const double* __restrict__ kv, double alpha,
+                                           size_t e) {
+  double w = __ldg(nv + e);
+  if (kv) w = __dadd_rn(w, __dmul_rn(alpha, __ldg(kv + e)));
+  return w;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// pass A: column transforms (+ column sums for the loss)
+// ---------------------------------------------------------------------------
+struct PassAArgs {
+  const double* X;
+  const double* nv;
+  const double* kv;
+  double alpha;
+  double2* T;
+  double* dots;
+  const double2* tw;
+  const double2* tabK;
+  const double2* tabLlo;
+  const double2* tabLhi;
+  int d, N2, K_rows, nblk, want_T;
+  int res_base[MAXRES], res_cnt[MAXRES];
+};
+
+template <int N1>
+__global__ void __launch_bounds__(256) passA_kernel(const PassAArgs a) {
+  constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1);
+  extern __shared__ double2 smem[];
+  __shared__ double red[2][256];
+  const int G = blockDim.x / T;
+  const int tid = threadIdx.x, g = tid / T, t = tid - g * T;
+  const int n2 = blockIdx.x * G + g;
+  const int pair = blockIdx.y;
+  const int d = a.d;
+  const size_t Np = (size_t)N1 * a.N2;
+  const double* xa = a.X + (size_t)(2 * pair) * Np + (size_t)n2 * N1;
+  const double* xb = xa + Np;
+  const size_t eoff = (size_t)n2 * N1;
+
+  cplx z[E];
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int n1 = t + T * r;
+    const double w = state_at(a.nv, a.kv, a.alpha, eoff + n1);
+    const double va = __ldg(xa + n1) * w, vb = __ldg(xb + n1) * w;
+    z[r] = mk(va, vb);
+    sa += va;
+    sb += vb;
+  }
+  // deterministic block reduction of the column sums (any block size)
+  __syncthreads();
+  red[0][tid] = sa;
+  red[1][tid] = sb;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w && tid + w < (int)blockDim.x) {
+      red[0][tid] += red[0][tid + w];
+      red[1][tid] += red[1][tid + w];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.dots[(size_t)(2 * pair) * a.nblk + blockIdx.x] = red[0][0];
+    a.dots[(size_t)(2 * pair + 1) * a.nblk + blockIdx.x] = red[1][0];
+  }
+  if (!a.want_T) return;
+
+  double2* exch = smem + g * SE;
+  double2* ybuf = smem + (G + g) * SE;
+  const size_t colT = (size_t)a.K_rows * a.N2;
+  double2* Ta = a.T + (size_t)(2 * pair) * colT + (size_t)n2 * 8;
+  double2* Tb = Ta + colT;
+
+  auto emit = [&](int j, int k1, cplx Z, cplx Zm) {
+    // Z = Zcol[kappa], Zm = Zcol[-kappa]; separate the two real columns
+    const int kappa = j + d * k1;
+    const cplx cz = cconj(Zm);
+    const cplx A = cscale(cadd(Z, cz), 0.5);
+    const cplx B = cscale(mul_mi(csub(Z, cz)), 0.5);
+    const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * kappa);
+    const int rho = a.res_base[j] + k1;
+    const size_t off = (size_t)(rho >> 3) * ((size_t)a.N2 * 8) + (rho & 7);
+    sts_c(Ta + off, cmul(A, w));
+    sts_c(Tb + off, cmul(B, w));
+  };
+
+  // residue 0 (self-mirrored): rows k1 in [0, N1/2]
+  {
+    cplx v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = z[r];
+    fft_fwd<N1>(v, t, exch, a.tw);
+#pragma unroll
+    for (int r = 0; r < E; ++r) sts_c(ybuf + pad16(t + T * r), v[r]);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int k1 = t + T * r;
+      if (k1 <= N1 / 2) emit(0, k1, v[r], lds_c(ybuf + pad16((N1 - k1) & (N1 - 1))));
+    }
+    __syncthreads();
+  }
+  // residue pairs (j, d-j), 0 < j < d/2: all rows of residue j
+  for (int j = 1; 2 * j < d; ++j) {
+    cplx v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = cmul(z[r], ld_c(a.tabK + j * (t + T * r)));
+    fft_fwd<N1>(v, t, exch, a.tw);
+#pragma unroll
+    for (int r = 0; r < E; ++r) sts_c(ybuf + pad16(t + T * r), v[r]);
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = cmul(z[r], ld_c(a.tabK + (d - j) * (t + T * r)));
+    fft_fwd<N1>(v, t, exch, a.tw);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int k1 = N1 - 1 - (t + T * r);
+      emit(j, k1, lds_c(ybuf + pad16(k1)), v[r]);
+    }
+    __syncthreads();
+  }
+  // residue d/2 (even d, self-mirrored): rows k1 in [0, N1/2)
+  if ((d & 1) == 0) {
+    const int j = d / 2;
+    cplx v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = cmul(z[r], ld_c(a.tabK + j * (t + T * r)));
+    fft_fwd<N1>(v, t, exch, a.tw);
+#pragma unroll
+    for (int r = 0; r < E; ++r) sts_c(ybuf + pad16(t + T * r), v[r]);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int k1 = t + T * r;
+      if (2 * k1 < N1) emit(j, k1, v[r], lds_c(ybuf + pad16(N1 - 1 - k1)));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass B: row FFTs, spectral product / chain, inverse row FFTs
+// ---------------------------------------------------------------------------
+struct PassBArgs {
+  const double2* T;
+  double2* U;
+  const double2* tw;
+  const double2* tabLlo;
+  const double2* tabLhi;
+  const int* rowkappa;
+  double2* scratch;
+  long long L;
+  int d, K, K_rows, C, kind, Rmax;
+  int ranks[MAXD + 1];
+};
+
+template <int N2, bool TT>
+__global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
+  constexpr int E = fft_e(N2), T = fft_t(N2), SE = fft_smem_elems(N2);
+  constexpr int ROWS = 128 / T;
+  extern __shared__ double2 smem[];
+  const int tid = threadIdx.x;
+  const int rl8 = tid & 7, t = (tid >> 3) % T, sub = (tid >> 3) / T;
+  const int rloc = sub * 8 + rl8;
+  const int rho = blockIdx.x * ROWS + rloc;
+  const bool valid = rho < a.K_rows;
+  double2* exch = smem + rloc * SE;
+  const size_t colT = (size_t)a.K_rows * N2;
+  const double2* Tb = a.T + (size_t)(rho >> 3) * (N2 * 8) + (rho & 7);
+
+  cplx S[E], prod[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    S[i] = mk(0.0, 0.0);
+    prod[i] = mk(0.0, 0.0);
+  }
+  const int d = a.d;
+
+  if constexpr (!TT) {
+    int m = 0;
+    for (int c = 0; c < a.C; ++c) {
+      cplx v[E];
+      const double2* src = Tb + (size_t)c * colT;
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (t + T * i) * 8) : mk(0.0, 0.0);
+      fft_fwd<N2>(v, t, exch, a.tw);
+      if (m == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) prod[i] = v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) prod[i] = cmul(prod[i], v[i]);
+      }
+      if (m == d - 1) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) S[i] = cadd(S[i], prod[i]);
+        m = 0;
+      } else {
+        ++m;
+      }
+    }
+  } else {
+    // TT chain; state vectors in a private global scratch (coalesced per thread slot)
+    const size_t slot = (size_t)blockIdx.x * 2 * a.Rmax;
+    auto st = [&](int b, int r, int i) -> double2* {
+      return a.scratch + ((slot + (size_t)b * a.Rmax + r) * E + i) * blockDim.x + tid;
+    };
+    int c = 0, in = 0;
+    for (int lam = 0; lam < d; ++lam) {
+      const int rp_n = a.ranks[lam], rn_n = a.ranks[lam + 1];
+      for (int rn = 0; rn < rn_n; ++rn) {
+        for (int rp = 0; rp < rp_n; ++rp, ++c) {
+          cplx v[E];
+          const double2* src = Tb + (size_t)c * colT;
+#pragma unroll
+          for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (t + T * i) * 8) : mk(0.0, 0.0);
+          fft_fwd<N2>(v, t, exch, a.tw);
+          if (lam == 0) {
+#pragma unroll
+            for (int i = 0; i < E; ++i) sts_c(st(in, rn, i), v[i]);
+          } else {
+            if (rp == 0) {
+#pragma unroll
+              for (int i = 0; i < E; ++i) prod[i] = mk(0.0, 0.0);
+            }
+#pragma unroll
+            for (int i = 0; i < E; ++i) prod[i] = cadd(prod[i], cmul(lds_c(st(in, rp, i)), v[i]));
+            if (rp == rp_n - 1) {
+              if (lam == d - 1) {
+#pragma unroll
+                for (int i = 0; i < E; ++i) S[i] = prod[i];
+              } else {
+#pragma unroll
+                for (int i = 0; i < E; ++i) sts_c(st(in ^ 1, rn, i), prod[i]);
+              }
+            }
+          }
+        }
+      }
+      if (lam > 0) in ^= 1;
+    }
+  }
+
+  // (d-1)-position shift (s'[t] = s[t-(d-1)] <=> S'[k] = S[k] W_L^{(d-1)k}), inverse row FFT, inverse twiddle, Hermitian weight
+  const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const long long k = (long long)kap + (long long)a.K * (t + T * i);
+    const long long m = ((long long)(d - 1) * k) % a.L;
+    S[i] = cmul(S[i], twL(a.tabLlo, a.tabLhi, m));  // shift by d-1: * W_L^{+(d-1)k}
+  }
+  fft_inv<N2>(S, t, exch, a.tw);
+  const double wgt = (kap == 0 || 2 * kap == a.K) ? 1.0 : 2.0;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int n2 = t + T * i;
+      const cplx u = cscale(cmulc(S[i], twL(a.tabLlo, a.tabLhi, (long long)n2 * kap)), wgt);
+      sts_c(a.U + (size_t)n2 * a.K_rows + rho, u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pass C: inverse column transforms, pruned to the sizes 1..N
+// ---------------------------------------------------------------------------
+struct PassCArgs {
+  const double2* U;
+  double* p;
+  const double2* tw;
+  const double2* tabK;
+  long long N;
+  double invL, fact;
+  int d, N2, K_rows, nres;
+  int res_base[MAXRES], res_cnt[MAXRES];
+};
+
+template <int N1>
+__global__ void __launch_bounds__(256) passC_kernel(const PassCArgs a) {
+  constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1);
+  extern __shared__ double2 smem[];
+  const int G = blockDim.x / T;
+  const int tid = threadIdx.x, g = tid / T, t = tid - g * T;
+  const int n2 = blockIdx.x * G + g;
+  double2* exch = smem + g * SE;
+  const double2* Ucol = a.U + (size_t)n2 * a.K_rows;
+  double acc[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) acc[r] = 0.0;
+  for (int j = 0; j < a.nres; ++j) {
+    cplx v[E];
+    const int cnt = a.res_cnt[j];
+    const double2* src = Ucol + a.res_base[j];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int k1 = t + T * r;
+      v[r] = k1 < cnt ? ld_c(src + k1) : mk(0.0, 0.0);
+    }
+    fft_inv<N1>(v, t, exch, a.tw);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const cplx w = ld_c(a.tabK + j * (t + T * r));
+      acc[r] += w.x * v[r].x + w.y * v[r].y;  // Re(conj(W^(j n1)) v)
+    }
+  }
+  double* dst = a.p + (size_t)n2 * N1;
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int n1 = t + T * r;
+    const long long o = (long long)n1 * a.N2 + n2;
+    dst[n1] = (o >= a.d - 1 && o < a.N) ? (acc[r] * a.invL) / a.fact : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// loss coefficients: ordered reduction of the pass-A column sums
+// ---------------------------------------------------------------------------
+struct QArgs {
+  const double* dots;
+  double* coef;
+  int nblk, C, kind, d, R;
+  int ranks[MAXD + 1];
+  int core_off[MAXD + 1];
+};
+
+__global__ void qcoef_kernel(const QArgs a) {
+  extern __shared__ double sdot[];
+  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+    double s = 0.0;
+    const double* p = a.dots + (size_t)c * a.nblk;
+    for (int b = 0; b < a.nblk; ++b) s += p[b];
+    sdot[c] = s;
+  }
+  __syncthreads();
+  if (a.kind == TTAGG_KIND_CP) {
+    // s_r = prod_{m < d-1} <F^(m)[:, r], n>   (rhs.py:401-412)
+    for (int r = threadIdx.x; r < a.R; r += blockDim.x) {
+      double s = 1.0;
+      for (int m = 0; m < a.d - 1; ++m) s *= sdot[r * a.d + m];
+      a.coef[r] = s;
+    }
+  } else if (threadIdx.x == 0) {
+    // w = V1 V2 ... V_{d-1}, V_l[rp, rn] = sum_i H_l[rp, i, rn] n_i   (rhs.py:305-338)
+    double w[64], wn[64];
+    for (int rn = 0; rn < a.ranks[1]; ++rn) w[rn] = sdot[a.core_off[0] + rn];
+    for (int lam = 1; lam < a.d - 1; ++lam) {
+      const int rp_n = a.ranks[lam], rn_n = a.ranks[lam + 1];
+      for (int rn = 0; rn < rn_n; ++rn) {
+        double s = 0.0;
+        for (int rp = 0; rp < rp_n; ++rp) s += w[rp] * sdot[a.core_off[lam] + rn * rp_n + rp];
+        wn[rn] = s;
+      }
+      for (int rn = 0; rn < rn_n; ++rn) w[rn] = wn[rn];
+    }
+    for (int rp = 0; rp < a.ranks[a.d - 1]; ++rp) a.coef[rp] = w[rp];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// combine: sum orders, loss tail, outputs / fused RK2 stage
+// ---------------------------------------------------------------------------
+struct CombineOrder {
+  const double* p;     // perm-layout gain (nullable)
+  const double* X;     // columns (perm layout)
+  const int* tail;     // tail column indices
+  const double* coef;  // tail coefficients (nullable -> no loss)
+  int ntail;
+  double qdiv;  // (d-1)!
+};
+
+struct CombineArgs {
+  CombineOrder o[MAXORD];
+  int nord;
+  const double* nv;
+  const double* kv;
+  double alpha;
+  long long N;
+  int N1, N2;
+  // natural outputs
+  double* p;
+  double* q;
+  double* s;
+  // perm outputs
+  double* out_perm;     // s or base + a*s
+  const double* base;   // stage base (nullable -> out = s)
+  double a;
+  double* diagp;        // per-block partials (nullable)
+};
+
+__device__ __forceinline__ void pq_at(const CombineArgs& A, size_t e, double nvv, double& P, double& Q) {
+  const size_t Np = (size_t)A.N1 * A.N2;
+  P = 0.0;
+  Q = 0.0;
+  for (int k = 0; k < A.nord; ++k) {
+    const CombineOrder& o = A.o[k];
+    if (o.p) P += __ldg(o.p + e);
+    if (o.coef) {
+      double tail = 0.0;
+      for (int r = 0; r < o.ntail; ++r) tail += __ldg(o.X + (size_t)__ldg(o.tail + r) * Np + e) * __ldg(o.coef + r);
+      Q += -(nvv * tail) / o.qdiv;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) combine_natural_kernel(const CombineArgs A) {
+  __shared__ double tp[32][33], tq[32][33];
+  const int TN1 = min(32, A.N1), TN2 = min(32, A.N2);
+  const int n1_0 = blockIdx.y * TN1, n2_0 = blockIdx.x * TN2;
+  for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
+    const int i1 = idx % TN1, i2 = idx / TN1;
+    const size_t e = (size_t)(n2_0 + i2) * A.N1 + (n1_0 + i1);
+    double P, Q;
+    pq_at(A, e, state_at(A.nv, A.kv, A.alpha, e), P, Q);
+    tp[i2][i1] = P;
+    tq[i2][i1] = Q;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
+    const int i2 = idx % TN2, i1 = idx / TN2;
+    const long long o = (long long)(n1_0 + i1) * A.N2 + (n2_0 + i2);
+    if (o < A.N) {
+      const double P = tp[i2][i1], Q = tq[i2][i1];
+      if (A.p) A.p[o] = P;
+      if (A.q) A.q[o] = Q;
+      if (A.s) A.s[o] = P + Q;
+    }
+  }
+}
+
+// diag partial layout per block: [0] nonfinite count, [1] min, [2] max|.|, [3..5] M0..M2
+constexpr int DIAGW = 8;
+
+__global__ void __launch_bounds__(256) combine_perm_kernel(const CombineArgs A) {
+  __shared__ double red[6][8];
+  const size_t Np = (size_t)A.N1 * A.N2;
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double nf = 0.0, mn = INFINITY, mx = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  if (e < Np) {
+    const int n1 = (int)(e % A.N1), n2 = (int)(e / A.N1);
+    const long long o = (long long)n1 * A.N2 + n2;
+    double out = 0.0;
+    if (o < A.N) {
+      const double nvv = state_at(A.nv, A.kv, A.alpha, e);
+      double P, Q;
+      pq_at(A, e, nvv, P, Q);
+      const double s = P + Q;
+      out = A.base ? __dadd_rn(__ldg(A.base + e), __dmul_rn(A.a, s)) : s;
+      if (A.diagp) {
+        nf = isfinite(out) ? 0.0 : 1.0;
+        mn = out;
+        mx = fabs(out);
+        const double k = (double)(o + 1);
+        m0 = out;
+        m1 = k * out;
+        m2 = k * k * out;
+      }
+    }
+    A.out_perm[e] = out;
+  }
+  if (!A.diagp) return;
+  // deterministic block reduction
+  nf = warp_sum(nf);
+  m0 = warp_sum(m0);
+  m1 = warp_sum(m1);
+  m2 = warp_sum(m2);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = nf; red[1][wid] = mn; red[2][wid] = mx;
+    red[3][wid] = m0; red[4][wid] = m1; red[5][wid] = m2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v[6] = {0.0, INFINITY, 0.0, 0.0, 0.0, 0.0};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      v[0] += red[0][w]; v[1] = fmin(v[1], red[1][w]); v[2] = fmax(v[2], red[2][w]);
+      v[3] += red[3][w]; v[4] += red[4][w]; v[5] += red[5][w];
+    }
+    double* dst = A.diagp + (size_t)blockIdx.x * DIAGW;
+    for (int i = 0; i < 6; ++i) dst[i] = v[i];
+  }
+}
+
+// elementwise stage out = base + a*s with diagnostics (multi-GPU path, after the all-reduce)
+__global__ void __launch_bounds__(256) stage_kernel(const double* base, const double* s, double a, double* out,
+                                                    long long N, int N1, int N2, double* diagp) {
+  __shared__ double red[6][8];
+  const size_t Np = (size_t)N1 * N2;
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double nf = 0.0, mn = INFINITY, mx = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  if (e < Np) {
+    const int n1 = (int)(e % N1), n2 = (int)(e / N1);
+    const long long o = (long long)n1 * N2 + n2;
+    double v = 0.0;
+    if (o < N) {
+      v = base ? __dadd_rn(base[e], __dmul_rn(a, s[e])) : s[e];
+      nf = isfinite(v) ? 0.0 : 1.0;
+      mn = v;
+      mx = fabs(v);
+      const double k = (double)(o + 1);
+      m0 = v; m1 = k * v; m2 = k * k * v;
+    }
+    if (out) out[e] = v;
+  }
+  if (!diagp) return;
+  nf = warp_sum(nf); m0 = warp_sum(m0); m1 = warp_sum(m1); m2 = warp_sum(m2);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = nf; red[1][wid] = mn; red[2][wid] = mx;
+    red[3][wid] = m0; red[4][wid] = m1; red[5][wid] = m2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v[6] = {0.0, INFINITY, 0.0, 0.0, 0.0, 0.0};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      v[0] += red[0][w]; v[1] = fmin(v[1], red[1][w]); v[2] = fmax(v[2], red[2][w]);
+      v[3] += red[3][w]; v[4] += red[4][w]; v[5] += red[5][w];
+    }
+    double* dst = diagp + (size_t)blockIdx.x * DIAGW;
+    for (int i = 0; i < 6; ++i) dst[i] = v[i];
+  }
+}
+
+// fixed-order reduction of the per-block partials -> diag[0..5]
+__global__ void diag_finalize_kernel(const double* diagp, int nb, double* diag) {
+  __shared__ double red[6][256];
+  double v[6] = {0.0, INFINITY, 0.0, 0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const double* p = diagp + (size_t)b * DIAGW;
+    v[0] += p[0]; v[1] = fmin(v[1], p[1]); v[2] = fmax(v[2], p[2]);
+    v[3] += p[3]; v[4] += p[4]; v[5] += p[5];
+  }
+  for (int i = 0; i < 6; ++i) red[i][threadIdx.x] = v[i];
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + w];
+      red[1][threadIdx.x] = fmin(red[1][threadIdx.x], red[1][threadIdx.x + w]);
+      red[2][threadIdx.x] = fmax(red[2][threadIdx.x], red[2][threadIdx.x + w]);
+      red[3][threadIdx.x] += red[3][threadIdx.x + w];
+      red[4][threadIdx.x] += red[4][threadIdx.x + w];
+      red[5][threadIdx.x] += red[5][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 6; ++i) diag[i] = red[i][0];
+}
+
+// RK2 bookkeeping after one step (device-resident, integrator.py:207-227):
+// book[0] = current step, [1] = fail step, [2] = negativity step, [3] = rows written
+__global__ void rk2_book_kernel(const double* diag_mid, const double* diag_new, int64_t* book, long long record_every,
+                                double* rec) {
+  if (threadIdx.x != 0) return;
+  const long long step = book[0] + 1;
+  book[0] = step;
+  if (book[1] != 0) return;
+  if (diag_mid[0] != 0.0 || diag_new[0] != 0.0) {
+    book[1] = step;
+    return;
+  }
+  if (book[2] == 0 && diag_new[1] < -1e-9 * diag_new[2]) book[2] = step;
+  if (step % record_every == 0) {
+    const long long row = book[3];
+    rec[row * 4 + 0] = diag_new[3];
+    rec[row * 4 + 1] = diag_new[4];
+    rec[row * 4 + 2] = diag_new[5];
+    rec[row * 4 + 3] = diag_new[1];
+    book[3] = row + 1;
+  }
+}
+
+__global__ void rk2_book_init_kernel(const double* diag0, int64_t* book, double* rec) {
+  if (threadIdx.x != 0) return;
+  book[0] = 0; book[1] = 0; book[2] = 0; book[3] = 1;
+  rec[0] = diag0[3]; rec[1] = diag0[4]; rec[2] = diag0[5]; rec[3] = diag0[1];
+}
+
+// ---------------------------------------------------------------------------
+// layout kernels
+// ---------------------------------------------------------------------------
+// dir 0: natural (length N) -> perm (length Np, zero padded); dir 1: perm -> natural
+__global__ void permute_kernel(const double* __restrict__ in, double* __restrict__ out, long long N, int N1, int N2,
+                               int dir) {
+  __shared__ double tile[32][33];
+  const int TN1 = min(32, N1), TN2 = min(32, N2);
+  const int n1_0 = blockIdx.y * TN1, n2_0 = blockIdx.x * TN2;
+  if (dir == 0) {
+    // read natural: consecutive threads -> consecutive n2
+    for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
+      const int i2 = idx % TN2, i1 = idx / TN2;
+      const long long o = (long long)(n1_0 + i1) * N2 + (n2_0 + i2);
+      tile[i2][i1] = o < N ? in[o] : 0.0;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
+      const int i1 = idx % TN1, i2 = idx / TN1;
+      out[(size_t)(n2_0 + i2) * N1 + (n1_0 + i1)] = tile[i2][i1];
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
+      const int i1 = idx % TN1, i2 = idx / TN1;
+      tile[i2][i1] = in[(size_t)(n2_0 + i2) * N1 + (n1_0 + i1)];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
+      const int i2 = idx % TN2, i1 = idx / TN2;
+      const long long o = (long long)(n1_0 + i1) * N2 + (n2_0 + i2);
+      if (o < N) out[o] = tile[i2][i1];
+    }
+  }
+}
+
+// scatter an N x R row-major factor (or a TT core slice) into perm-layout columns
+// column of (rank index j) goes to X[colmap[j]]; src element (o, j) at src[o*ld + j*jstride + off]
+__global__ void scatter_columns_kernel(const double* __restrict__ src, long long N, int ld, int ncols,
+                                       const int* __restrict__ srcidx, const int* __restrict__ colmap, double* X,
+                                       int N1, int N2) {
+  const size_t Np = (size_t)N1 * N2;
+  const int j = blockIdx.y;
+  const int sj = srcidx[j];
+  double* dst = X + (size_t)colmap[j] * Np;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < Np; e += (size_t)gridDim.x * blockDim.x) {
+    const int n1 = (int)(e % N1), n2 = (int)(e / N1);
+    const long long o = (long long)n1 * N2 + n2;
+    dst[e] = o < N ? src[o * ld + sj] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: plans, workspaces, launches
+// ---------------------------------------------------------------------------
+int ensure(void** p, size_t* have, size_t need, bool zero = false) {
+  if (*have >= need) return TTAGG_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  size_t alloc = std::max<size_t>(need, 256);
+  cudaError_t e = cudaMalloc(p, alloc);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TTAGG_ERR_NOMEM, "device allocation of " + std::to_string(alloc) + " bytes failed: " + cudaGetErrorString(e));
+  }
+  if (zero) CUDA_TRY(cudaMemset(*p, 0, alloc));
+  *have = alloc;
+  return TTAGG_OK;
+}
+
+int get_plan(ttagg_ctx* ctx, int d, const Geom& g, OrderPlan** out) {
+  auto key = std::make_pair(d, g.Np);
+  auto it = ctx->plans.find(key);
+  if (it != ctx->plans.end()) {
+    *out = it->second;
+    return TTAGG_OK;
+  }
+  OrderPlan* P = new OrderPlan();
+  P->d = d;
+  P->g = g;
+  P->L = (int64_t)d * g.Np;
+  P->K = d * g.N1;
+  const int N1 = g.N1;
+  int base = 0, nres = 0;
+  auto add = [&](int cnt) {
+    P->res_base[nres] = base;
+    P->res_cnt[nres] = cnt;
+    base += (cnt + 7) & ~7;
+    ++nres;
+  };
+  add(N1 / 2 + 1);
+  for (int j = 1; 2 * j < d; ++j) add(N1);
+  if ((d & 1) == 0) add(N1 / 2);
+  P->nres = nres;
+  P->K_rows = base;
+  std::vector<int> kap(P->K_rows, -1);
+  for (int j = 0; j < nres; ++j)
+    for (int k1 = 0; k1 < P->res_cnt[j]; ++k1) kap[P->res_base[j] + k1] = j + d * k1;
+  std::vector<double2> tk, tlo, thi;
+  host_twiddles(tk, P->K, P->K, 1);
+  host_twiddles(tlo, P->L, LLO, 1);
+  const int64_t nhi = (P->L + LLO - 1) / LLO;
+  host_twiddles(thi, P->L, nhi, LLO);
+  auto up = [&](void** dst, const void* src, size_t bytes) -> int {
+    CUDA_TRY(cudaMalloc(dst, bytes));
+    CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+    return TTAGG_OK;
+  };
+  TRY(up((void**)&P->tabK, tk.data(), tk.size() * sizeof(double2)));
+  TRY(up((void**)&P->tabLlo, tlo.data(), tlo.size() * sizeof(double2)));
+  TRY(up((void**)&P->tabLhi, thi.data(), thi.size() * sizeof(double2)));
+  TRY(up((void**)&P->rowkappa, kap.data(), kap.size() * sizeof(int)));
+  ctx->plans[key] = P;
+  *out = P;
+  return TTAGG_OK;
+}
+
+// raise the dynamic shared-memory cap once per kernel instantiation (never
+// inside a stream capture: the first launch of every shape runs eagerly)
+template <typename K>
+int set_smem(K kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> done;  // per kernel instantiation
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[(const void*)kern];
+  if (bytes > 48 * 1024 && bytes > have) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+  }
+  return TTAGG_OK;
+}
+
+// ---- pass A
+template <int N1>
+int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
+  constexpr int T = fft_t(N1);
+  const int G = std::min(256 / T, N2);
+  const size_t smem = (size_t)2 * G * fft_smem_elems(N1) * sizeof(double2);
+  TRY(set_smem(passA_kernel<N1>, smem));
+  dim3 grid(N2 / G, npairs);
+  passA_kernel<N1><<<grid, T * G, smem, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return TTAGG_OK;
+}
+
+int nblk_for(int N1, int N2) {
+  const int T = fft_t(N1);
+  const int G = std::min(256 / T, N2);
+  return N2 / G;
+}
+
+int dispatchA(int N1, const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
+  switch (N1) {
+    case 4: return launchA<4>(a, N2, npairs, st);
+    case 8: return launchA<8>(a, N2, npairs, st);
+    case 16: return launchA<16>(a, N2, npairs, st);
+    case 32: return launchA<32>(a, N2, npairs, st);
+    case 64: return launchA<64>(a, N2, npairs, st);
+    case 128: return launchA<128>(a, N2, npairs, st);
+    case 256: return launchA<256>(a, N2, npairs, st);
+    case 512: return launchA<512>(a, N2, npairs, st);
+    case 1024: return launchA<1024>(a, N2, npairs, st);
+    case 2048: return launchA<2048>(a, N2, npairs, st);
+    case 4096: return launchA<4096>(a, N2, npairs, st);
+  }
+  return fail(TTAGG_ERR_UNSUPPORTED, "unsupported N1");
+}
+
+// ---- pass B
+template <int N2, bool TT>
+int launchB(const PassBArgs& a, cudaStream_t st) {
+  constexpr int T = fft_t(N2);
+  constexpr int ROWS = 128 / T;
+  const size_t smem = (size_t)ROWS * fft_smem_elems(N2) * sizeof(double2);
+  TRY(set_smem(passB_kernel<N2, TT>, smem));
+  const int grid = (a.K_rows + ROWS - 1) / ROWS;
+  passB_kernel<N2, TT><<<grid, 128, smem, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return TTAGG_OK;
+}
+
+int rowsB(int N2) { return 128 / fft_t(N2); }
+
+int dispatchB(int N2, bool tt, const PassBArgs& a, cudaStream_t st) {
+#define TTAGG_B(n) \
+  case n: return tt ? launchB<n, true>(a, st) : launchB<n, false>(a, st);
+  switch (N2) {
+    TTAGG_B(16)
+    TTAGG_B(32)
+    TTAGG_B(64)
+    TTAGG_B(128)
+    TTAGG_B(256)
+  }
+#undef TTAGG_B
+  return fail(TTAGG_ERR_UNSUPPORTED, "unsupported N2");
+}
+
+// ---- pass C
+template <int N1>
+int launchC(const PassCArgs& a, int N2, cudaStream_t st) {
+  constexpr int T = fft_t(N1);
+  const int G = std::min(256 / T, N2);
+  const size_t smem = (size_t)G * fft_smem_elems(N1) * sizeof(double2);
+  TRY(set_smem(passC_kernel<N1>, smem));
+  passC_kernel<N1><<<N2 / G, T * G, smem, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return TTAGG_OK;
+}
+
+int dispatchC(int N1, const PassCArgs& a, int N2, cudaStream_t st) {
+  switch (N1) {
+    case 4: return launchC<4>(a, N2, st);
+    case 8: return launchC<8>(a, N2, st);
+    case 16: return launchC<16>(a, N2, st);
+    case 32: return launchC<32>(a, N2, st);
+    case 64: return launchC<64>(a, N2, st);
+    case 128: return launchC<128>(a, N2, st);
+    case 256: return launchC<256>(a, N2, st);
+    case 512: return launchC<512>(a, N2, st);
+    case 1024: return launchC<1024>(a, N2, st);
+    case 2048: return launchC<2048>(a, N2, st);
+    case 4096: return launchC<4096>(a, N2, st);
+  }
+  return fail(TTAGG_ERR_UNSUPPORTED, "unsupported N1");
+}
+
+// profiling helpers
+cudaEvent_t prof_event(ttagg_ctx* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  ttagg_ctx* ctx;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(ttagg_ctx* c, int k, cudaStream_t s) : ctx(c), cls(k), st(s) {
+    if (ctx->prof) {
+      a = prof_event(ctx);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (ctx->prof) {
+      cudaEvent_t b = prof_event(ctx);
+      cudaEventRecord(b, st);
+      ctx->recs.push_back({cls, a, b});
+    }
+  }
+};
+
+// Evaluate the gain of one kernel into pbuf slot and/or its loss coefficients.
+int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const double* kv, double alpha, bool wantP,
+              bool wantQ, double* p_out, cudaStream_t st) {
+  const OrderPlan* P = k->plan;
+  const Geom& g = k->g;
+  const int npairs = k->C_pad / 2;
+  if (npairs > 65535) return fail(TTAGG_ERR_UNSUPPORTED, "too many columns for one kernel");
+  if (wantP) {
+    const size_t need = (size_t)k->C_pad * P->K_rows * g.N2 * sizeof(double2);
+    TRY(ensure((void**)&ctx->T, &ctx->T_bytes, need, true));
+    TRY(ensure((void**)&ctx->U, &ctx->U_bytes, (size_t)P->K_rows * g.N2 * sizeof(double2)));
+  }
+  PassAArgs a{};
+  a.X = k->X;
+  a.nv = nv;
+  a.kv = kv;
+  a.alpha = alpha;
+  a.T = ctx->T;
+  a.dots = k->dots;
+  a.tw = ctx->tw4096;
+  a.tabK = P->tabK;
+  a.tabLlo = P->tabLlo;
+  a.tabLhi = P->tabLhi;
+  a.d = k->d;
+  a.N2 = g.N2;
+  a.K_rows = P->K_rows;
+  a.nblk = k->nblk;
+  a.want_T = wantP ? 1 : 0;
+  for (int j = 0; j < MAXRES; ++j) {
+    a.res_base[j] = P->res_base[j];
+    a.res_cnt[j] = P->res_cnt[j];
+  }
+  {
+    ProfScope ps(ctx, 0, st);
+    TRY(dispatchA(g.N1, a, g.N2, npairs, st));
+  }
+  if (wantQ) {
+    QArgs q{};
+    q.dots = k->dots;
+    q.coef = k->coef;
+    q.nblk = k->nblk;
+    q.C = k->C;
+    q.kind = k->kind;
+    q.d = k->d;
+    q.R = k->R;
+    for (int i = 0; i <= MAXD; ++i) {
+      q.ranks[i] = k->ranks[i];
+      q.core_off[i] = k->core_off[i];
+    }
+    ProfScope ps(ctx, 3, st);
+    qcoef_kernel<<<1, 256, std::max(1, k->C_pad) * sizeof(double), st>>>(q);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (wantP) {
+    PassBArgs b{};
+    b.T = ctx->T;
+    b.U = ctx->U;
+    b.tw = ctx->tw4096;
+    b.tabLlo = P->tabLlo;
+    b.tabLhi = P->tabLhi;
+    b.rowkappa = P->rowkappa;
+    b.L = P->L;
+    b.d = k->d;
+    b.K = P->K;
+    b.K_rows = P->K_rows;
+    b.C = k->C;
+    b.kind = k->kind;
+    b.Rmax = k->Rmax;
+    for (int i = 0; i <= MAXD; ++i) b.ranks[i] = k->ranks[i];
+    if (k->kind == TTAGG_KIND_TT) {
+      const int rows = rowsB(g.N2);
+      const int grid = (P->K_rows + rows - 1) / rows;
+      const size_t need = (size_t)grid * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
+      TRY(ensure((void**)&ctx->scratch, &ctx->scratch_bytes, need));
+      b.scratch = ctx->scratch;
+    }
+    {
+      ProfScope ps(ctx, 1, st);
+      TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, st));
+    }
+    PassCArgs c{};
+    c.U = ctx->U;
+    c.p = p_out;
+    c.tw = ctx->tw4096;
+    c.tabK = P->tabK;
+    c.N = g.N;
+    c.invL = 1.0 / (double)P->L;
+    double f = 1.0;
+    for (int i = 2; i <= k->d; ++i) f *= i;
+    c.fact = f;
+    c.d = k->d;
+    c.N2 = g.N2;
+    c.K_rows = P->K_rows;
+    c.nres = P->nres;
+    for (int j = 0; j < MAXRES; ++j) {
+      c.res_base[j] = P->res_base[j];
+      c.res_cnt[j] = P->res_cnt[j];
+    }
+    ProfScope ps(ctx, 2, st);
+    TRY(dispatchC(g.N1, c, g.N2, st));
+  }
+  return TTAGG_OK;
+}
+
+int check_set(const ttagg_kernel* const* ks, int nk, Geom* g) {
+  if (nk <= 0 || !ks) return fail(TTAGG_ERR_EMPTY, "no collision orders configured");
+  if (nk > MAXORD) return fail(TTAGG_ERR_UNSUPPORTED, "too many orders");
+  for (int i = 0; i < nk; ++i) {
+    if (!ks[i]) return fail(TTAGG_ERR_ARG, "null kernel");
+    if (ks[i]->N != ks[0]->N) return fail(TTAGG_ERR_SIZE, "all kernels in a set must share the same N");
+  }
+  *g = ks[0]->g;
+  return TTAGG_OK;
+}
+
+// Run all orders: gains into pbuf, loss coefficients; fill the combine descriptor.
+int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const double* nv, const double* kv,
+               double alpha, bool wantP, bool wantQ, CombineArgs* A, cudaStream_t st) {
+  const Geom& g = ks[0]->g;
+  if (wantP) TRY(ensure((void**)&ctx->pbuf, &ctx->pbuf_bytes, (size_t)nk * g.Np * sizeof(double)));
+  for (int i = 0; i < nk; ++i) {
+    const ttagg_kernel* k = ks[i];
+    double* pslot = wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr;
+    TRY(run_order(ctx, k, nv, kv, alpha, wantP, wantQ, pslot, st));
+    CombineOrder& o = A->o[i];
+    o.p = pslot;
+    o.X = k->X;
+    o.tail = k->tail_cols;
+    o.coef = wantQ ? k->coef : nullptr;
+    o.ntail = k->ntail;
+    double f = 1.0;
+    for (int j = 2; j <= k->d - 1; ++j) f *= j;
+    o.qdiv = f;
+  }
+  A->nord = nk;
+  A->nv = nv;
+  A->kv = kv;
+  A->alpha = alpha;
+  A->N = g.N;
+  A->N1 = g.N1;
+  A->N2 = g.N2;
+  return TTAGG_OK;
+}
+
+int launch_permute(const double* in, double* out, const Geom& g, int dir, cudaStream_t st) {
+  const int TN1 = std::min(32, g.N1), TN2 = std::min(32, g.N2);
+  dim3 grid(g.N2 / TN2, g.N1 / TN1);
+  permute_kernel<<<grid, 256, 0, st>>>(in, out, g.N, g.N1, g.N2, dir);
+  CUDA_TRY(cudaGetLastError());
+  return TTAGG_OK;
+}
+
+int launch_combine_perm(CombineArgs& A, const Geom& g, cudaStream_t st) {
+  const int nb = (int)((g.Np + 255) / 256);
+  combine_perm_kernel<<<nb, 256, 0, st>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  return TTAGG_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int ttagg_version(void) { return 10000 * 0 + 100 * 1 + 0; }
+
+const char* ttagg_last_error(void) { return g_err.c_str(); }
+
+int ttagg_geometry(int64_t n_classes, int64_t* out3) {
+  Geom g;
+  TRY(make_geom(n_classes, &g));
+  out3[0] = g.Np;
+  out3[1] = g.N1;
+  out3[2] = g.N2;
+  return TTAGG_OK;
+}
+
+int ttagg_ctx_create(int device, ttagg_ctx** out) {
+  if (!out) return fail(TTAGG_ERR_ARG, "null out");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(TTAGG_ERR_ARG, "bad device index");
+  CUDA_TRY(cudaSetDevice(device));
+  ttagg_ctx* ctx = new ttagg_ctx();
+  ctx->device = device;
+  std::vector<double2> tw;
+  host_twiddles(tw, TW_BASE, TW_BASE, 1);
+  CUDA_TRY(cudaMalloc(&ctx->tw4096, TW_BASE * sizeof(double2)));
+  CUDA_TRY(cudaMemcpy(ctx->tw4096, tw.data(), TW_BASE * sizeof(double2), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&ctx->diag, 4 * DIAGW * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&ctx->book, 8 * sizeof(int64_t)));
+  *out = ctx;
+  return TTAGG_OK;
+}
+
+int ttagg_ctx_destroy(ttagg_ctx* ctx) {
+  if (!ctx) return TTAGG_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : ctx->plans) {
+    OrderPlan* P = kv.second;
+    cudaFree(P->tabK);
+    cudaFree(P->tabLlo);
+    cudaFree(P->tabLhi);
+    cudaFree(P->rowkappa);
+    delete P;
+  }
+  cudaFree(ctx->tw4096);
+  cudaFree(ctx->T);
+  cudaFree(ctx->U);
+  cudaFree(ctx->pbuf);
+  cudaFree(ctx->scratch);
+  cudaFree(ctx->vec);
+  cudaFree(ctx->diagp);
+  cudaFree(ctx->diag);
+  cudaFree(ctx->book);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& r : ctx->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  delete ctx;
+  return TTAGG_OK;
+}
+
+static int finish_upload(ttagg_ctx* ctx, ttagg_kernel* k, const std::vector<int>& tails) {
+  k->ntail = (int)tails.size();
+  CUDA_TRY(cudaMalloc(&k->tail_cols, std::max<size_t>(1, tails.size()) * sizeof(int)));
+  if (!tails.empty())
+    CUDA_TRY(cudaMemcpy(k->tail_cols, tails.data(), tails.size() * sizeof(int), cudaMemcpyHostToDevice));
+  k->nblk = nblk_for(k->g.N1, k->g.N2);
+  CUDA_TRY(cudaMalloc(&k->dots, (size_t)std::max(2, k->C_pad) * k->nblk * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&k->coef, std::max<size_t>(1, tails.size()) * sizeof(double)));
+  TRY(get_plan(ctx, k->d, k->g, &k->plan));
+  return TTAGG_OK;
+}
+
+int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, const double* const* factors,
+                    const int64_t* rank_subset, int64_t n_subset, ttagg_kernel** out) {
+  if (!ctx || !out || !factors) return fail(TTAGG_ERR_ARG, "null argument");
+  if (d < 2) return fail(TTAGG_ERR_ARG, "a CP kernel needs at least two factors");
+  if (d > MAXD) return fail(TTAGG_ERR_UNSUPPORTED, "collision order above 8");
+  if (rank < 1) return fail(TTAGG_ERR_ARG, "CP factors must be N x R matrices with R >= 1");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(make_geom(n_classes, &g));
+  std::vector<int> sel;
+  if (rank_subset) {
+    for (int64_t i = 0; i < n_subset; ++i) {
+      if (rank_subset[i] < 0 || rank_subset[i] >= rank) return fail(TTAGG_ERR_ARG, "rank index out of range");
+      sel.push_back((int)rank_subset[i]);
+    }
+  } else {
+    for (int64_t r = 0; r < rank; ++r) sel.push_back((int)r);
+  }
+  ttagg_kernel* k = new ttagg_kernel();
+  k->ctx = ctx;
+  k->kind = TTAGG_KIND_CP;
+  k->d = d;
+  k->N = n_classes;
+  k->g = g;
+  k->R = (int)sel.size();
+  k->C = d * k->R;
+  k->C_pad = (k->C + 1) & ~1;
+  k->Rmax = 1;
+  const size_t colbytes = (size_t)g.Np * sizeof(double);
+  {
+    cudaError_t e = cudaMalloc(&k->X, std::max<size_t>(2, k->C_pad) * colbytes);
+    if (e != cudaSuccess) {
+      delete k;
+      return fail(TTAGG_ERR_NOMEM, "factor upload allocation failed");
+    }
+  }
+  CUDA_TRY(cudaMemset(k->X, 0, std::max<size_t>(2, k->C_pad) * colbytes));
+  std::vector<int> tails;
+  if (k->R > 0) {
+    double* dsrc = nullptr;
+    int *dsel = nullptr, *dmap = nullptr;
+    CUDA_TRY(cudaMalloc(&dsrc, (size_t)n_classes * rank * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&dsel, sel.size() * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&dmap, sel.size() * sizeof(int)));
+    CUDA_TRY(cudaMemcpy(dsel, sel.data(), sel.size() * sizeof(int), cudaMemcpyHostToDevice));
+    for (int m = 0; m < d; ++m) {
+      if (!factors[m]) return fail(TTAGG_ERR_ARG, "null factor");
+      CUDA_TRY(cudaMemcpy(dsrc, factors[m], (size_t)n_classes * rank * sizeof(double), cudaMemcpyHostToDevice));
+      std::vector<int> map(sel.size());
+      for (size_t j = 0; j < sel.size(); ++j) map[j] = (int)j * d + m;  // rank-major column order
+      CUDA_TRY(cudaMemcpy(dmap, map.data(), map.size() * sizeof(int), cudaMemcpyHostToDevice));
+      dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)sel.size());
+      scatter_columns_kernel<<<grid, 256>>>(dsrc, n_classes, (int)rank, (int)sel.size(), dsel, dmap, k->X, g.N1, g.N2);
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(dsrc);
+    cudaFree(dsel);
+    cudaFree(dmap);
+    for (int j = 0; j < k->R; ++j) tails.push_back(j * d + d - 1);
+  }
+  TRY(finish_upload(ctx, k, tails));
+  *out = k;
+  return TTAGG_OK;
+}
+
+int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ranks, const double* const* cores,
+                    ttagg_kernel** out) {
+  if (!ctx || !out || !cores || !ranks) return fail(TTAGG_ERR_ARG, "null argument");
+  if (d < 2) return fail(TTAGG_ERR_ARG, "a TT kernel needs at least two cores");
+  if (d > MAXD) return fail(TTAGG_ERR_UNSUPPORTED, "collision order above 8");
+  if (ranks[0] != 1 || ranks[d] != 1) return fail(TTAGG_ERR_ARG, "boundary TT ranks must equal 1");
+  for (int l = 0; l <= d; ++l)
+    if (ranks[l] < 1) return fail(TTAGG_ERR_ARG, "TT ranks must be >= 1");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(make_geom(n_classes, &g));
+  ttagg_kernel* k = new ttagg_kernel();
+  k->ctx = ctx;
+  k->kind = TTAGG_KIND_TT;
+  k->d = d;
+  k->N = n_classes;
+  k->g = g;
+  int C = 0, Rmax = 1;
+  for (int l = 0; l <= d; ++l) {
+    k->ranks[l] = (int)ranks[l];
+    Rmax = std::max(Rmax, (int)ranks[l]);
+  }
+  if (Rmax > 64) {
+    delete k;
+    return fail(TTAGG_ERR_UNSUPPORTED, "TT ranks above 64");
+  }
+  for (int l = 0; l < d; ++l) {
+    k->core_off[l] = C;
+    C += k->ranks[l] * k->ranks[l + 1];
+  }
+  k->core_off[d] = C;
+  k->C = C;
+  k->C_pad = (C + 1) & ~1;
+  k->Rmax = Rmax;
+  k->R = k->ranks[d - 1];
+  const size_t colbytes = (size_t)g.Np * sizeof(double);
+  CUDA_TRY(cudaMalloc(&k->X, std::max<size_t>(2, k->C_pad) * colbytes));
+  CUDA_TRY(cudaMemset(k->X, 0, std::max<size_t>(2, k->C_pad) * colbytes));
+  double* dsrc = nullptr;
+  int *dsel = nullptr, *dmap = nullptr;
+  size_t maxcore = 0;
+  for (int l = 0; l < d; ++l) maxcore = std::max(maxcore, (size_t)k->ranks[l] * n_classes * k->ranks[l + 1]);
+  CUDA_TRY(cudaMalloc(&dsrc, maxcore * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&dsel, 64 * 64 * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&dmap, 64 * 64 * sizeof(int)));
+  for (int l = 0; l < d; ++l) {
+    if (!cores[l]) return fail(TTAGG_ERR_ARG, "null core");
+    const int rp_n = k->ranks[l], rn_n = k->ranks[l + 1];
+    CUDA_TRY(cudaMemcpy(dsrc, cores[l], (size_t)rp_n * n_classes * rn_n * sizeof(double), cudaMemcpyHostToDevice));
+    // element H[rp, o, rn] at rp*N*rn_n + o*rn_n + rn.  Handle one rp slab at a time:
+    for (int rp = 0; rp < rp_n; ++rp) {
+      std::vector<int> sidx(rn_n), map(rn_n);
+      for (int rn = 0; rn < rn_n; ++rn) {
+        sidx[rn] = rn;
+        map[rn] = k->core_off[l] + rn * rp_n + rp;  // fiber order: rn-major, rp inner
+      }
+      CUDA_TRY(cudaMemcpy(dsel, sidx.data(), rn_n * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(dmap, map.data(), rn_n * sizeof(int), cudaMemcpyHostToDevice));
+      dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)rn_n);
+      scatter_columns_kernel<<<grid, 256>>>(dsrc + (size_t)rp * n_classes * rn_n, n_classes, rn_n, rn_n, dsel, dmap,
+                                            k->X, g.N1, g.N2);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaDeviceSynchronize());
+    }
+  }
+  cudaFree(dsrc);
+  cudaFree(dsel);
+  cudaFree(dmap);
+  std::vector<int> tails;
+  for (int rp = 0; rp < k->ranks[d - 1]; ++rp) tails.push_back(k->core_off[d - 1] + rp);
+  TRY(finish_upload(ctx, k, tails));
+  *out = k;
+  return TTAGG_OK;
+}
+
+int ttagg_kernel_free(ttagg_kernel* k) {
+  if (!k) return TTAGG_OK;
+  cudaSetDevice(k->ctx->device);
+  cudaDeviceSynchronize();
+  cudaFree(k->X);
+  cudaFree(k->tail_cols);
+  cudaFree(k->dots);
+  cudaFree(k->coef);
+  delete k;
+  return TTAGG_OK;
+}
+
+int ttagg_kernel_info(const ttagg_kernel* k, int64_t* info) {
+  if (!k || !info) return fail(TTAGG_ERR_ARG, "null argument");
+  info[0] = k->kind;
+  info[1] = k->d;
+  info[2] = k->N;
+  info[3] = k->C;
+  info[4] = k->g.Np;
+  info[5] = k->g.N1;
+  info[6] = k->g.N2;
+  info[7] = k->plan ? k->plan->K_rows : 0;
+  return TTAGG_OK;
+}
+
+int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels, const double* n, double* p,
+              double* q, double* s, int flags, void* stream) {
+  if (!ctx || !n) return fail(TTAGG_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(check_set(kernels, n_kernels, &g));
+  cudaStream_t st = (cudaStream_t)stream;
+  bool wantP = flags & TTAGG_WANT_P, wantQ = flags & TTAGG_WANT_Q;
+  if (!wantP && !wantQ) wantP = wantQ = true;
+  const bool host = flags & TTAGG_HOST_PTRS;
+  // vec layout: [n natural N][n perm Np][p N][q N][s N]
+  const size_t nb = (size_t)g.N * sizeof(double), pb = (size_t)g.Np * sizeof(double);
+  TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, 4 * nb + pb + 1024));
+  double* v_nat = ctx->vec;
+  double* v_perm = v_nat + g.N;
+  double* v_p = v_perm + g.Np;
+  double* v_q = v_p + g.N;
+  double* v_s = v_q + g.N;
+  const double* nsrc = n;
+  if (host) {
+    for (int64_t i = 0; i < g.N; ++i)
+      if (!std::isfinite(n[i])) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
+    CUDA_TRY(cudaMemcpyAsync(v_nat, n, nb, cudaMemcpyHostToDevice, st));
+    nsrc = v_nat;
+  }
+  TRY(launch_permute(nsrc, v_perm, g, 0, st));
+  CombineArgs A{};
+  TRY(run_orders(ctx, kernels, n_kernels, v_perm, nullptr, 0.0, wantP, wantQ, &A, st));
+  A.p = p ? (host ? v_p : p) : nullptr;
+  A.q = q ? (host ? v_q : q) : nullptr;
+  A.s = s ? (host ? v_s : s) : nullptr;
+  {
+    ProfScope ps(ctx, 3, st);
+    const int TN1 = std::min(32, g.N1), TN2 = std::min(32, g.N2);
+    dim3 grid(g.N2 / TN2, g.N1 / TN1);
+    combine_natural_kernel<<<grid, 256, 0, st>>>(A);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (host) {
+    if (p) CUDA_TRY(cudaMemcpyAsync(p, v_p, nb, cudaMemcpyDeviceToHost, st));
+    if (q) CUDA_TRY(cudaMemcpyAsync(q, v_q, nb, cudaMemcpyDeviceToHost, st));
+    if (s) CUDA_TRY(cudaMemcpyAsync(s, v_s, nb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return TTAGG_OK;
+}
+
+int ttagg_rhs_perm(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels, const double* n_perm,
+                   const double* k_perm, double alpha, double* s_perm, void* stream) {
+  if (!ctx || !n_perm || !s_perm) return fail(TTAGG_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(check_set(kernels, n_kernels, &g));
+  cudaStream_t st = (cudaStream_t)stream;
+  CombineArgs A{};
+  TRY(run_orders(ctx, kernels, n_kernels, n_perm, k_perm, alpha, true, true, &A, st));
+  A.out_perm = s_perm;
+  A.base = nullptr;
+  A.diagp = nullptr;
+  ProfScope ps(ctx, 3, st);
+  TRY(launch_combine_perm(A, g, st));
+  return TTAGG_OK;
+}
+
+int ttagg_permute(ttagg_ctx* ctx, int64_t n_classes, const double* in, double* out, int dir, void* stream) {
+  if (!ctx || !in || !out) return fail(TTAGG_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(make_geom(n_classes, &g));
+  return launch_permute(in, out, g, dir ? 1 : 0, (cudaStream_t)stream);
+}
+
+int ttagg_stage(ttagg_ctx* ctx, int64_t n_classes, const double* base, const double* s, double a, double* out,
+                double* diag, void* stream) {
+  if (!ctx || !s) return fail(TTAGG_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(make_geom(n_classes, &g));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = (int)((g.Np + 255) / 256);
+  double* dp = nullptr;
+  if (diag) {
+    TRY(ensure((void**)&ctx->diagp, &ctx->diagp_bytes, (size_t)nb * DIAGW * sizeof(double)));
+    dp = ctx->diagp;
+  }
+  stage_kernel<<<nb, 256, 0, st>>>(base, s, a, out, g.N, g.N1, g.N2, dp);
+  CUDA_TRY(cudaGetLastError());
+  if (diag) {
+    diag_finalize_kernel<<<1, 256, 0, st>>>(dp, nb, diag);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return TTAGG_OK;
+}
+
+int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels, double* n_inout, double t0,
+              double dt, int64_t steps, int64_t record_every, double* records, int64_t* fail_step,
+              int64_t* neg_step, int flags, void* stream) {
+  (void)t0;
+  if (!ctx || !n_inout || !records || !fail_step || !neg_step) return fail(TTAGG_ERR_ARG, "null argument");
+  if (!(dt > 0)) return fail(TTAGG_ERR_ARG, "dt must be positive");
+  if (steps < 1 || record_every < 1) return fail(TTAGG_ERR_ARG, "steps and record_every must be >= 1");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(check_set(kernels, n_kernels, &g));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool host = flags & TTAGG_HOST_PTRS;
+  const int64_t nrows = steps / record_every + 1;
+  // vec layout: [nat N][A Np][B Np][C Np][rec nrows*4]
+  const size_t nb = (size_t)g.N * sizeof(double), pb = (size_t)g.Np * sizeof(double);
+  TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, nb + 3 * pb + (size_t)nrows * 4 * sizeof(double) + 1024));
+  double* v_nat = ctx->vec;
+  double* vA = v_nat + g.N;
+  double* vB = vA + g.Np;
+  double* vC = vB + g.Np;
+  double* rec = vC + g.Np;
+  const int nblk = (int)((g.Np + 255) / 256);
+  TRY(ensure((void**)&ctx->diagp, &ctx->diagp_bytes, (size_t)2 * nblk * DIAGW * sizeof(double)));
+  double* dpm = ctx->diagp;
+  double* dpn = ctx->diagp + (size_t)nblk * DIAGW;
+  double* dmid = ctx->diag;
+  double* dnew = ctx->diag + DIAGW;
+  double* d0 = ctx->diag + 2 * DIAGW;
+  if (host) {
+    for (int64_t i = 0; i < g.N; ++i)
+      if (!std::isfinite(n_inout[i])) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
+    CUDA_TRY(cudaMemcpyAsync(v_nat, n_inout, nb, cudaMemcpyHostToDevice, st));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(v_nat, n_inout, nb, cudaMemcpyDeviceToDevice, st));
+  }
+  TRY(launch_permute(v_nat, vA, g, 0, st));
+  // initial record
+  stage_kernel<<<nblk, 256, 0, st>>>(vA, vA, 0.0, nullptr, g.N, g.N1, g.N2, dpn);
+  diag_finalize_kernel<<<1, 256, 0, st>>>(dpn, nblk, d0);
+  rk2_book_init_kernel<<<1, 32, 0, st>>>(d0, ctx->book, rec);
+  CUDA_TRY(cudaGetLastError());
+
+  double* cur = vA;
+  double* mid = vB;
+  double* nxt = vC;
+  // one step: k1 -> mid = n + dt/2 k1 ; k2 at mid -> nxt = n + dt k2
+  auto step_once = [&](double* n_cur, double* n_mid, double* n_nxt) -> int {
+    CombineArgs A{};
+    TRY(run_orders(ctx, kernels, n_kernels, n_cur, nullptr, 0.0, true, true, &A, st));
+    A.out_perm = n_mid;
+    A.base = n_cur;
+    A.a = 0.5 * dt;
+    A.diagp = dpm;
+    TRY(launch_combine_perm(A, g, st));
+    diag_finalize_kernel<<<1, 256, 0, st>>>(dpm, nblk, dmid);
+    CombineArgs B{};
+    TRY(run_orders(ctx, kernels, n_kernels, n_mid, nullptr, 0.0, true, true, &B, st));
+    B.out_perm = n_nxt;
+    B.base = n_cur;
+    B.a = dt;
+    B.diagp = dpn;
+    TRY(launch_combine_perm(B, g, st));
+    diag_finalize_kernel<<<1, 256, 0, st>>>(dpn, nblk, dnew);
+    rk2_book_kernel<<<1, 32, 0, st>>>(dmid, dnew, ctx->book, record_every, rec);
+    CUDA_TRY(cudaGetLastError());
+    return TTAGG_OK;
+  };
+  // capture one step for each buffer parity into CUDA graphs
+  const bool use_graph = !ctx->prof;
+  cudaGraphExec_t ge[2] = {nullptr, nullptr};
+  cudaStream_t cap = st;
+  bool own_stream = false;
+  if (use_graph && st == nullptr) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    own_stream = true;
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  int64_t host_book[4] = {0, 0, 0, 0};
+  int rc = TTAGG_OK;
+  if (use_graph) {
+    // make sure workspaces exist before capture (allocation is not capturable)
+    st = cap;
+    TRY(step_once(cur, mid, nxt));  // step 1 runs eagerly
+    std::swap(cur, nxt);
+    for (int par = 0; par < 2 && steps > 1; ++par) {
+      double* c0 = par == 0 ? cur : nxt;
+      double* c1 = par == 0 ? nxt : cur;
+      cudaGraph_t gr;
+      CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      rc = step_once(c0, mid, c1);
+      cudaError_t ec = cudaStreamEndCapture(cap, &gr);
+      if (rc) return rc;
+      if (ec != cudaSuccess) return fail(TTAGG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+      CUDA_TRY(cudaGraphInstantiate(&ge[par], gr, 0));
+      cudaGraphDestroy(gr);
+    }
+    int64_t done = 1;
+    int par = 0;
+    while (done < steps) {
+      const int64_t chunk = std::min<int64_t>(steps - done, 64);
+      for (int64_t i = 0; i < chunk; ++i) {
+        CUDA_TRY(cudaGraphLaunch(ge[par], cap));
+        par ^= 1;
+      }
+      done += chunk;
+      CUDA_TRY(cudaMemcpyAsync(host_book, ctx->book, sizeof(host_book), cudaMemcpyDeviceToHost, cap));
+      CUDA_TRY(cudaStreamSynchronize(cap));
+      if (host_book[1] != 0) break;
+    }
+    if (par == 1) std::swap(cur, nxt);  // final state location
+    for (auto& e : ge)
+      if (e) cudaGraphExecDestroy(e);
+  } else {
+    for (int64_t s = 1; s <= steps; ++s) {
+      TRY(step_once(cur, mid, nxt));
+      std::swap(cur, nxt);
+      if (s % 64 == 0 || s == steps) {
+        CUDA_TRY(cudaMemcpyAsync(host_book, ctx->book, sizeof(host_book), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (host_book[1] != 0) break;
+      }
+    }
+  }
+  CUDA_TRY(cudaMemcpyAsync(host_book, ctx->book, sizeof(host_book), cudaMemcpyDeviceToHost, cap));
+  TRY(launch_permute(cur, v_nat, g, 1, cap));
+  // records: device rows (M0, M1, M2, min) -> (t, M0, M1, M2, min) with t filled by the caller
+  std::vector<double> hrec((size_t)nrows * 4);
+  CUDA_TRY(cudaMemcpyAsync(hrec.data(), rec, hrec.size() * sizeof(double), cudaMemcpyDeviceToHost, cap));
+  if (host) {
+    CUDA_TRY(cudaMemcpyAsync(n_inout, v_nat, nb, cudaMemcpyDeviceToHost, cap));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(n_inout, v_nat, nb, cudaMemcpyDeviceToDevice, cap));
+  }
+  CUDA_TRY(cudaStreamSynchronize(cap));
+  if (own_stream) cudaStreamDestroy(cap);
+  const int64_t rows = host_book[3];
+  std::vector<double> out((size_t)nrows * 5, 0.0);
+  for (int64_t r = 0; r < rows && r < nrows; ++r)
+    for (int c = 0; c < 4; ++c) out[r * 5 + 1 + c] = hrec[r * 4 + c];
+  if (host) {
+    std::memcpy(records, out.data(), out.size() * sizeof(double));
+  } else {
+    CUDA_TRY(cudaMemcpy(records, out.data(), out.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  *fail_step = host_book[1];
+  *neg_step = host_book[2];
+  return TTAGG_OK;
+}
+
+int ttagg_profile_enable(ttagg_ctx* ctx, int on) {
+  if (!ctx) return fail(TTAGG_ERR_ARG, "null ctx");
+  ctx->prof = on != 0;
+  return TTAGG_OK;
+}
+
+int ttagg_profile_read(ttagg_ctx* ctx, double* out5) {
+  if (!ctx || !out5) return fail(TTAGG_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  double acc[5] = {0, 0, 0, 0, 0};
+  for (auto& r : ctx->recs) {
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+    acc[r.cls] += ms;
+    if (r.cls == 0 || r.cls == 1 || r.cls == 2) acc[4] += (r.cls == 1) ? 1.0 : 0.0;
+    ctx->ev_pool.push_back(r.a);
+    ctx->ev_pool.push_back(r.b);
+  }
+  ctx->recs.clear();
+  for (int i = 0; i < 5; ++i) out5[i] = acc[i];
+  return TTAGG_OK;
+}
+
+}  // extern "C"
