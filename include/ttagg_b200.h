@@ -126,13 +126,19 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
               double* records, int64_t* fail_step, int64_t* neg_step, int flags,
               void* stream);
 
-/* Per-launch timing of the dominant kernel for the roofline report:
- * after ttagg_profile_enable(ctx, 1), ttagg_rhs* records CUDA events around
- * every launch of the gain FFT kernels; ttagg_profile_read returns
- * {pass1_ms, pass2_ms, pass3_ms, other_ms, launches} accumulated since the
- * last read (5 doubles). */
+/* Per-launch timing for the roofline report: after
+ * ttagg_profile_enable(ctx, 1) every launch issued by ttagg_rhs / ttagg_rhs_perm
+ * is bracketed by CUDA events on its stream.  ttagg_profile_read fills
+ * out72[(cls*9 + d)*2 + {0: milliseconds, 1: launches}] accumulated since
+ * the last read; cls 0 = pass A (column FFTs), 1 = pass B (row FFTs +
+ * spectral product), 2 = pass C (inverse column FFTs), 3 = other (loss
+ * coefficients, combine); d = collision order (0 for order-free launches). */
 int ttagg_profile_enable(ttagg_ctx* ctx, int on);
-int ttagg_profile_read(ttagg_ctx* ctx, double* out5);
+int ttagg_profile_read(ttagg_ctx* ctx, double* out72);
+
+/* Number of kernel launches this context has issued from ttagg_rhs /
+ * ttagg_rhs_perm (monotone counter; the bench reports the difference). */
+int ttagg_launch_count(ttagg_ctx* ctx, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -85,6 +85,7 @@ _SIGNATURES = {
     ),
     "ttagg_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ttagg_profile_read": (ctypes.c_int, [_vp, _c_double_p]),
+    "ttagg_launch_count": (ctypes.c_int, [_vp, _c_int64_p]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -306,10 +307,22 @@ class Context:
     def profile(self, on: bool):
         check(load().ttagg_profile_enable(self.handle, 1 if on else 0), "ttagg_profile_enable")
 
+    def launch_count(self) -> int:
+        out = ctypes.c_int64(0)
+        check(load().ttagg_launch_count(self.handle, ctypes.byref(out)), "ttagg_launch_count")
+        return int(out.value)
+
     def profile_read(self):
-        out = (ctypes.c_double * 5)()
+        """{(cls, d): (ms, launches)} since the last read; cls 0/1/2/3 = pass A/B/C/other."""
+        out = (ctypes.c_double * 72)()
         check(load().ttagg_profile_read(self.handle, out), "ttagg_profile_read")
-        return [float(x) for x in out]
+        res = {}
+        for cls in range(4):
+            for d in range(9):
+                ms, cnt = out[(cls * 9 + d) * 2], out[(cls * 9 + d) * 2 + 1]
+                if cnt:
+                    res[(cls, d)] = (float(ms), int(cnt))
+        return res
 
 
 _CONTEXTS: dict[int, Context] = {}

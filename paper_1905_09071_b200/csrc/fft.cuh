@@ -173,6 +173,43 @@ __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
 constexpr int TW_BASE = 4096;  // twiddle table W_4096^m
 
+// Barrier used between FFT stages: the whole CTA, or a named barrier over
+// one thread group (bar.sync id, nthreads; id 0 is __syncthreads).
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct WarpSync {  // all threads of one transform live in one warp (T <= 32)
+  __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
+struct GroupSync {
+  int id, n;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  }
+};
+
+// x[i] *= w^i for i = 1..15 with w^1, w^4 loaded: the other powers need at
+// most two multiplications from a table value (keeps twiddles within ~2 ulp)
+__device__ __forceinline__ void twiddle16(cplx* x, cplx w1, cplx w4) {
+  const cplx w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+  const cplx w8 = cmul(w4, w4), w12 = cmul(w8, w4);
+  x[1] = cmul(x[1], w1);
+  x[2] = cmul(x[2], w2);
+  x[3] = cmul(x[3], w3);
+  x[4] = cmul(x[4], w4);
+  x[5] = cmul(x[5], cmul(w4, w1));
+  x[6] = cmul(x[6], cmul(w4, w2));
+  x[7] = cmul(x[7], cmul(w4, w3));
+  x[8] = cmul(x[8], w8);
+  x[9] = cmul(x[9], cmul(w8, w1));
+  x[10] = cmul(x[10], cmul(w8, w2));
+  x[11] = cmul(x[11], cmul(w8, w3));
+  x[12] = cmul(x[12], w12);
+  x[13] = cmul(x[13], cmul(w12, w1));
+  x[14] = cmul(x[14], cmul(w12, w2));
+  x[15] = cmul(x[15], cmul(w12, w3));
+}
+
 // One stage.  Registers: element t + T*r in v[r] on entry (read pattern).
 template <int M, int R, int NS, bool LAST>
 __device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw) {
@@ -186,12 +223,26 @@ __device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* s
 #pragma unroll
     for (int i = 0; i < R; ++i) x[i] = v[u + i * G];
     if constexpr (NS > 1) {
+      // W_{NS R}^{i qm} = W_4096^{i qm 4096/(NS R)}
       const int qm = q & (NS - 1);
+      const int e = qm * (TW_BASE / (NS * R));
+#ifndef TTAGG_TW_MODE
+#define TTAGG_TW_MODE 0
+#endif
+      if constexpr (R == 16 && TTAGG_TW_MODE == 0) {
+        twiddle16(x, ld_c(tw + e), ld_c(tw + 4 * e));
+      } else if constexpr (R == 16 && TTAGG_TW_MODE == 2) {
+        // w1..w3 and w4, w8, w12 loaded; 9 products
+        const cplx w1 = ld_c(tw + e), w2 = ld_c(tw + 2 * e), w3 = ld_c(tw + 3 * e);
+        const cplx w4 = ld_c(tw + 4 * e), w8 = ld_c(tw + 8 * e), w12 = ld_c(tw + 12 * e);
+        x[1] = cmul(x[1], w1); x[2] = cmul(x[2], w2); x[3] = cmul(x[3], w3);
+        x[4] = cmul(x[4], w4); x[8] = cmul(x[8], w8); x[12] = cmul(x[12], w12);
+        x[5] = cmul(x[5], cmul(w4, w1)); x[6] = cmul(x[6], cmul(w4, w2)); x[7] = cmul(x[7], cmul(w4, w3));
+        x[9] = cmul(x[9], cmul(w8, w1)); x[10] = cmul(x[10], cmul(w8, w2)); x[11] = cmul(x[11], cmul(w8, w3));
+        x[13] = cmul(x[13], cmul(w12, w1)); x[14] = cmul(x[14], cmul(w12, w2)); x[15] = cmul(x[15], cmul(w12, w3));
+      } else {
 #pragma unroll
-      for (int i = 1; i < R; ++i) {
-        // W_{NS R}^{i qm} = W_4096^{i qm 4096/(NS R)}
-        const int idx = (i * qm) * (TW_BASE / (NS * R));
-        x[i] = cmul(x[i], ld_c(tw + idx));
+        for (int i = 1; i < R; ++i) x[i] = cmul(x[i], ld_c(tw + i * e));
       }
     }
     DFT<R>::run(x);
@@ -217,8 +268,9 @@ __device__ __forceinline__ void fft_load_regs(cplx (&v)[fft_e(M)], int t, const 
 // Forward FFT of length M (no normalisation).  All threads of the CTA must
 // call it (it contains __syncthreads when M > 16); `sm` is this transform's
 // private buffer of fft_smem_elems(M) slots.
-template <int M>
-__device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw) {
+template <int M, class Sync = CtaSync>
+__device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
+                                        const Sync& sync = Sync()) {
   if constexpr (M <= 16) {
     DFT<M>::run(v);
     // DFT<R> leaves natural order, and with T == 1 register r == frequency r
@@ -229,9 +281,9 @@ __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm,
     int ns_done;
     if constexpr (b > 1) {
       fft_stage<M, b, 1, false>(v, t, sm, tw);
-      __syncthreads();
+      sync();
       fft_load_regs<M>(v, t, sm);
-      __syncthreads();
+      sync();
     }
     constexpr int NS1 = b;
     // radix-16 stages: NS = b, 16 b, 256 b, ...
@@ -239,20 +291,20 @@ __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm,
       fft_stage<M, 16, NS1, true>(v, t, sm, tw);
     } else if constexpr (a == 2) {
       fft_stage<M, 16, NS1, false>(v, t, sm, tw);
-      __syncthreads();
+      sync();
       fft_load_regs<M>(v, t, sm);
-      __syncthreads();
+      sync();
       fft_stage<M, 16, NS1 * 16, true>(v, t, sm, tw);
     } else {
       static_assert(a == 3, "M <= 4096");
       fft_stage<M, 16, NS1, false>(v, t, sm, tw);
-      __syncthreads();
+      sync();
       fft_load_regs<M>(v, t, sm);
-      __syncthreads();
+      sync();
       fft_stage<M, 16, NS1 * 16, false>(v, t, sm, tw);
-      __syncthreads();
+      sync();
       fft_load_regs<M>(v, t, sm);
-      __syncthreads();
+      sync();
       fft_stage<M, 16, NS1 * 256, true>(v, t, sm, tw);
     }
     (void)ns_done;
@@ -260,12 +312,13 @@ __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm,
 }
 
 // Inverse (unnormalised) via conj(FFT(conj(x))).
-template <int M>
-__device__ __forceinline__ void fft_inv(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw) {
+template <int M, class Sync = CtaSync>
+__device__ __forceinline__ void fft_inv(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
+                                        const Sync& sync = Sync()) {
   constexpr int E = fft_e(M);
 #pragma unroll
   for (int r = 0; r < E; ++r) v[r].y = -v[r].y;
-  fft_fwd<M>(v, t, sm, tw);
+  fft_fwd<M, Sync>(v, t, sm, tw, sync);
 #pragma unroll
   for (int r = 0; r < E; ++r) v[r].y = -v[r].y;
 }

@@ -53,6 +53,7 @@ constexpr int MAXRES = MAXD / 2 + 1;
 constexpr int MAXORD = 8;
 constexpr int LSPLIT = 11;
 constexpr int LLO = 1 << LSPLIT;
+constexpr int RB = 4;  // residue row blocks are padded to multiples of RB rows
 
 thread_local std::string g_err;
 
@@ -87,6 +88,8 @@ int64_t next_pow2(int64_t x) {
 int make_geom(int64_t N, Geom* g) {
   if (N < 2) return fail(TTAGG_ERR_ARG, "concentration state must be a vector of length >= 2");
   int64_t Np = std::max<int64_t>(64, next_pow2(N));
+  // N = N1 x N2 with N2 <= 256 = 16^2 (row transforms: two radix-16 stages,
+  // 16 threads per row, warp-resident) and N1 <= 4096 = 16^3
   int64_t N1 = std::max<int64_t>(4, Np / 256);
   if (N1 > 4096)
     return fail(TTAGG_ERR_UNSUPPORTED, "N = " + std::to_string(N) + " exceeds the supported 2^20 size classes");
@@ -151,9 +154,10 @@ struct ttagg_ctx {
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
-  struct Rec { int cls; cudaEvent_t a, b; };
+  struct Rec { int cls, d; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   double prof_acc[5] = {0, 0, 0, 0, 0};
+  long long launches = 0;  // kernel launches issued by this context
 };
 
 struct ttagg_kernel {
@@ -216,118 +220,163 @@ struct PassAArgs {
   int res_base[MAXRES], res_cnt[MAXRES];
 };
 
+// One CTA = one column pair x G adjacent columns n2, run by two thread
+// groups of T*G threads (two residue FFTs in flight, named barriers); the
+// weighted input z = (a + i b) * n is staged once in shared memory.
 template <int N1>
-__global__ void __launch_bounds__(256) passA_kernel(const PassAArgs a) {
+__global__ void __launch_bounds__(512, 1) passA_kernel(const PassAArgs a) {
   constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1);
   extern __shared__ double2 smem[];
-  __shared__ double red[2][256];
-  const int G = blockDim.x / T;
-  const int tid = threadIdx.x, g = tid / T, t = tid - g * T;
+  __shared__ double red[2][512];
+  __shared__ double2 Pst[16];
+  const int GT = blockDim.x >> 1;  // threads per group
+  const int G = GT / T;            // columns per CTA
+  const int tid = threadIdx.x, grp = tid >= GT ? 1 : 0, lt = tid - grp * GT;
+  const int g = lt / T, t = lt - g * T;
   const int n2 = blockIdx.x * G + g;
   const int pair = blockIdx.y;
   const int d = a.d;
-  const size_t Np = (size_t)N1 * a.N2;
-  const double* xa = a.X + (size_t)(2 * pair) * Np + (size_t)n2 * N1;
-  const double* xb = xa + Np;
-  const size_t eoff = (size_t)n2 * N1;
+  double2* zbuf = smem;
+  double2* buf0 = smem + G * N1;
+  double2* buf1 = buf0 + G * SE;
+  double2* mybuf = (grp ? buf1 : buf0) + g * SE;
+  double2* otbuf = (grp ? buf0 : buf1) + g * SE;
+  const double2* zc = zbuf + g * N1;
 
-  cplx z[E];
-  double sa = 0.0, sb = 0.0;
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int n1 = t + T * r;
-    const double w = state_at(a.nv, a.kv, a.alpha, eoff + n1);
-    const double va = __ldg(xa + n1) * w, vb = __ldg(xb + n1) * w;
-    z[r] = mk(va, vb);
-    sa += va;
-    sb += vb;
-  }
-  // deterministic block reduction of the column sums (any block size)
-  __syncthreads();
-  red[0][tid] = sa;
-  red[1][tid] = sb;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (tid < w && tid + w < (int)blockDim.x) {
-      red[0][tid] += red[0][tid + w];
-      red[1][tid] += red[1][tid + w];
+  // stage z and reduce the column sums (loss operator), coalesced over G*N1
+  {
+    const size_t Np = (size_t)N1 * a.N2;
+    const size_t e0 = (size_t)blockIdx.x * G * N1;
+    const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
+    const double* xb = xa + Np;
+    double sa = 0.0, sb = 0.0;
+    const double2* xa2 = reinterpret_cast<const double2*>(xa);
+    const double2* xb2 = reinterpret_cast<const double2*>(xb);
+    const double2* nv2 = reinterpret_cast<const double2*>(a.nv + e0);
+    const double2* kv2 = a.kv ? reinterpret_cast<const double2*>(a.kv + e0) : nullptr;
+#pragma unroll 4
+    for (int i = tid; i < G * N1 / 2; i += blockDim.x) {
+      double2 w = __ldg(nv2 + i);
+      if (kv2) {
+        const double2 k = __ldg(kv2 + i);
+        w.x = __dadd_rn(w.x, __dmul_rn(a.alpha, k.x));
+        w.y = __dadd_rn(w.y, __dmul_rn(a.alpha, k.y));
+      }
+      const double2 ua = __ldg(xa2 + i), ub = __ldg(xb2 + i);
+      const double va0 = ua.x * w.x, va1 = ua.y * w.y, vb0 = ub.x * w.x, vb1 = ub.y * w.y;
+      zbuf[2 * i] = make_double2(va0, vb0);
+      zbuf[2 * i + 1] = make_double2(va1, vb1);
+      sa += va0 + va1;
+      sb += vb0 + vb1;
     }
+    red[0][tid] = sa;
+    red[1][tid] = sb;
     __syncthreads();
-  }
-  if (tid == 0) {
-    a.dots[(size_t)(2 * pair) * a.nblk + blockIdx.x] = red[0][0];
-    a.dots[(size_t)(2 * pair + 1) * a.nblk + blockIdx.x] = red[1][0];
+    for (int w = 256; w > 0; w >>= 1) {
+      if (tid < w && tid + w < (int)blockDim.x) {
+        red[0][tid] += red[0][tid + w];
+        red[1][tid] += red[1][tid + w];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      a.dots[(size_t)(2 * pair) * a.nblk + blockIdx.x] = red[0][0];
+      a.dots[(size_t)(2 * pair + 1) * a.nblk + blockIdx.x] = red[1][0];
+    }
   }
   if (!a.want_T) return;
+  // G == 1: row twiddle W_L^(n2 kappa) = base(thread, residue) * P[r], P[r] = W_L^(n2 d T r)
+  if (G == 1 && tid < 16) {
+    const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * tid);
+    Pst[tid] = make_double2(w.x, w.y);
+  }
+  __syncthreads();
 
-  double2* exch = smem + g * SE;
-  double2* ybuf = smem + (G + g) * SE;
   const size_t colT = (size_t)a.K_rows * a.N2;
-  double2* Ta = a.T + (size_t)(2 * pair) * colT + (size_t)n2 * 8;
+  double2* Ta = a.T + (size_t)(2 * pair) * colT + (size_t)n2 * a.K_rows;  // exchange layout T[c][n2][rho]
   double2* Tb = Ta + colT;
-
-  auto emit = [&](int j, int k1, cplx Z, cplx Zm) {
-    // Z = Zcol[kappa], Zm = Zcol[-kappa]; separate the two real columns
-    const int kappa = j + d * k1;
+  // w = W_L^(n2 kappa); separate the two real columns, twiddle, store
+  auto emit = [&](int j, int k1, cplx Z, cplx Zm, cplx w) {
     const cplx cz = cconj(Zm);
     const cplx A = cscale(cadd(Z, cz), 0.5);
     const cplx B = cscale(mul_mi(csub(Z, cz)), 0.5);
-    const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * kappa);
     const int rho = a.res_base[j] + k1;
-    const size_t off = (size_t)(rho >> 3) * ((size_t)a.N2 * 8) + (rho & 7);
+    const size_t off = rho;
     sts_c(Ta + off, cmul(A, w));
     sts_c(Tb + off, cmul(B, w));
   };
+  auto rowtw = [&](int kappa_base, int r, bool down) -> cplx {
+    // W_L^(n2 * (kappa_base +/- d*T*r))
+    if (G == 1) {
+      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kappa_base);
+      const cplx p = lds_c(Pst + r);
+      return down ? cmulc(b, p) : cmul(b, p);
+    }
+    const int kap = down ? kappa_base - d * T * r : kappa_base + d * T * r;
+    return twL(a.tabLlo, a.tabLhi, (long long)n2 * kap);
+  };
+  const GroupSync gs{1 + grp, GT};
 
-  // residue 0 (self-mirrored): rows k1 in [0, N1/2]
-  {
-    cplx v[E];
-#pragma unroll
-    for (int r = 0; r < E; ++r) v[r] = z[r];
-    fft_fwd<N1>(v, t, exch, a.tw);
-#pragma unroll
-    for (int r = 0; r < E; ++r) sts_c(ybuf + pad16(t + T * r), v[r]);
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int k1 = t + T * r;
-      if (k1 <= N1 / 2) emit(0, k1, v[r], lds_c(ybuf + pad16((N1 - k1) & (N1 - 1))));
-    }
-    __syncthreads();
-  }
-  // residue pairs (j, d-j), 0 < j < d/2: all rows of residue j
+  // residue pairs (j, d-j), 0 < j < d/2: group 0 transforms residue j,
+  // group 1 residue d-j; together they emit all N1 rows of residue j
   for (int j = 1; 2 * j < d; ++j) {
+    const int jr = grp ? d - j : j;
     cplx v[E];
 #pragma unroll
-    for (int r = 0; r < E; ++r) v[r] = cmul(z[r], ld_c(a.tabK + j * (t + T * r)));
-    fft_fwd<N1>(v, t, exch, a.tw);
-#pragma unroll
-    for (int r = 0; r < E; ++r) sts_c(ybuf + pad16(t + T * r), v[r]);
-#pragma unroll
-    for (int r = 0; r < E; ++r) v[r] = cmul(z[r], ld_c(a.tabK + (d - j) * (t + T * r)));
-    fft_fwd<N1>(v, t, exch, a.tw);
-    __syncthreads();
-#pragma unroll
     for (int r = 0; r < E; ++r) {
-      const int k1 = N1 - 1 - (t + T * r);
-      emit(j, k1, lds_c(ybuf + pad16(k1)), v[r]);
+      const int n1 = t + T * r;
+      v[r] = cmul(lds_c(zc + n1), ld_c(a.tabK + jr * n1));
+    }
+    fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
+#pragma unroll
+    for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
+    __syncthreads();
+    if (grp == 0) {
+      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * (j + d * t));
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const int k1 = t + T * r;
+        const cplx w = G == 1 ? cmul(b, lds_c(Pst + r)) : rowtw(j + d * t, r, false);
+        emit(j, k1, v[r], lds_c(otbuf + pad16(N1 - 1 - k1)), w);
+      }
+    } else {
+      const int kb = j + d * (N1 - 1 - t);
+      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kb);
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const int k1 = N1 - 1 - (t + T * r);
+        const cplx w = G == 1 ? cmulc(b, lds_c(Pst + r)) : rowtw(kb, r, true);
+        emit(j, k1, lds_c(otbuf + pad16(k1)), v[r], w);
+      }
     }
     __syncthreads();
   }
-  // residue d/2 (even d, self-mirrored): rows k1 in [0, N1/2)
-  if ((d & 1) == 0) {
-    const int j = d / 2;
-    cplx v[E];
+  // self-mirrored residues: 0 on group 0, d/2 (even d) on group 1
+  {
+    const int jr = grp == 0 ? 0 : ((d & 1) ? -1 : d / 2);
+    if (jr >= 0) {
+      cplx v[E];
 #pragma unroll
-    for (int r = 0; r < E; ++r) v[r] = cmul(z[r], ld_c(a.tabK + j * (t + T * r)));
-    fft_fwd<N1>(v, t, exch, a.tw);
+      for (int r = 0; r < E; ++r) {
+        const int n1 = t + T * r;
+        v[r] = jr == 0 ? lds_c(zc + n1) : cmul(lds_c(zc + n1), ld_c(a.tabK + jr * n1));
+      }
+      fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
 #pragma unroll
-    for (int r = 0; r < E; ++r) sts_c(ybuf + pad16(t + T * r), v[r]);
-    __syncthreads();
+      for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
+      if (GT >= 32) gs(); else __syncwarp();
+      const int kb = jr + d * t;
+      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kb);
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int k1 = t + T * r;
-      if (2 * k1 < N1) emit(j, k1, v[r], lds_c(ybuf + pad16(N1 - 1 - k1)));
+      for (int r = 0; r < E; ++r) {
+        const int k1 = t + T * r;
+        const bool keep = jr == 0 ? (2 * k1 <= N1) : (2 * k1 < N1);
+        if (keep) {
+          const cplx w = G == 1 ? cmul(b, lds_c(Pst + (r & 15))) : rowtw(kb, r, false);
+          const int mk = jr == 0 ? ((N1 - k1) & (N1 - 1)) : (N1 - 1 - k1);
+          emit(jr, k1, v[r], lds_c(mybuf + pad16(mk)), w);
+        }
+      }
     }
   }
 }
@@ -348,6 +397,17 @@ struct PassBArgs {
   int ranks[MAXD + 1];
 };
 
+__device__ __forceinline__ void cp_async16(double2* sdst, const double2* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NLEFT>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NLEFT) : "memory"); }
+
+// One CTA = 8 exchange rows x T threads per row (128 threads).  Lanes run
+// over the 8 rows fastest so every warp load reads whole 128-byte segments
+// of T[c][n2][rho]; the row transforms exchange through shared memory.
 template <int N2, bool TT>
 __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   constexpr int E = fft_e(N2), T = fft_t(N2), SE = fft_smem_elems(N2);
@@ -360,7 +420,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   const bool valid = rho < a.K_rows;
   double2* exch = smem + rloc * SE;
   const size_t colT = (size_t)a.K_rows * N2;
-  const double2* Tb = a.T + (size_t)(rho >> 3) * (N2 * 8) + (rho & 7);
+  const double2* Tb = a.T + rho;  // + c*colT + n2*K_rows
 
   cplx S[E], prod[E];
 #pragma unroll
@@ -369,14 +429,15 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     prod[i] = mk(0.0, 0.0);
   }
   const int d = a.d;
+  const int C = a.C;
 
   if constexpr (!TT) {
     int m = 0;
-    for (int c = 0; c < a.C; ++c) {
+    for (int c = 0; c < C; ++c) {
       cplx v[E];
       const double2* src = Tb + (size_t)c * colT;
 #pragma unroll
-      for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (t + T * i) * 8) : mk(0.0, 0.0);
+      for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
       fft_fwd<N2>(v, t, exch, a.tw);
       if (m == 0) {
 #pragma unroll
@@ -407,7 +468,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
           cplx v[E];
           const double2* src = Tb + (size_t)c * colT;
 #pragma unroll
-          for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (t + T * i) * 8) : mk(0.0, 0.0);
+          for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
           fft_fwd<N2>(v, t, exch, a.tw);
           if (lam == 0) {
 #pragma unroll
@@ -866,7 +927,7 @@ int get_plan(ttagg_ctx* ctx, int d, const Geom& g, OrderPlan** out) {
   auto add = [&](int cnt) {
     P->res_base[nres] = base;
     P->res_cnt[nres] = cnt;
-    base += (cnt + 7) & ~7;
+    base += (cnt + RB - 1) & ~(RB - 1);
     ++nres;
   };
   add(N1 / 2 + 1);
@@ -912,23 +973,22 @@ int set_smem(K kern, size_t bytes) {
 }
 
 // ---- pass A
+// columns per pass-A CTA: thread groups of <= 128 threads when the transform allows
+constexpr int passA_G(int T, int N2) { return std::max(1, std::min(128 / T, N2)); }
+
 template <int N1>
 int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   constexpr int T = fft_t(N1);
-  const int G = std::min(256 / T, N2);
-  const size_t smem = (size_t)2 * G * fft_smem_elems(N1) * sizeof(double2);
+  const int G = passA_G(T, N2);
+  const size_t smem = ((size_t)G * N1 + (size_t)2 * G * fft_smem_elems(N1)) * sizeof(double2);
   TRY(set_smem(passA_kernel<N1>, smem));
   dim3 grid(N2 / G, npairs);
-  passA_kernel<N1><<<grid, T * G, smem, st>>>(a);
+  passA_kernel<N1><<<grid, 2 * T * G, smem, st>>>(a);
   CUDA_TRY(cudaGetLastError());
   return TTAGG_OK;
 }
 
-int nblk_for(int N1, int N2) {
-  const int T = fft_t(N1);
-  const int G = std::min(256 / T, N2);
-  return N2 / G;
-}
+int nblk_for(int N1, int N2) { return N2 / passA_G(fft_t(N1), N2); }
 
 int dispatchA(int N1, const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   switch (N1) {
@@ -971,6 +1031,7 @@ int dispatchB(int N2, bool tt, const PassBArgs& a, cudaStream_t st) {
     TTAGG_B(64)
     TTAGG_B(128)
     TTAGG_B(256)
+    TTAGG_B(512)
   }
 #undef TTAGG_B
   return fail(TTAGG_ERR_UNSUPPORTED, "unsupported N2");
@@ -1019,10 +1080,10 @@ cudaEvent_t prof_event(ttagg_ctx* ctx) {
 
 struct ProfScope {
   ttagg_ctx* ctx;
-  int cls;
+  int cls, d;
   cudaStream_t st;
   cudaEvent_t a = nullptr;
-  ProfScope(ttagg_ctx* c, int k, cudaStream_t s) : ctx(c), cls(k), st(s) {
+  ProfScope(ttagg_ctx* c, int k, cudaStream_t s, int order = 0) : ctx(c), cls(k), d(order), st(s) {
     if (ctx->prof) {
       a = prof_event(ctx);
       cudaEventRecord(a, st);
@@ -1032,7 +1093,7 @@ struct ProfScope {
     if (ctx->prof) {
       cudaEvent_t b = prof_event(ctx);
       cudaEventRecord(b, st);
-      ctx->recs.push_back({cls, a, b});
+      ctx->recs.push_back({cls, d, a, b});
     }
   }
 };
@@ -1070,8 +1131,9 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
     a.res_cnt[j] = P->res_cnt[j];
   }
   {
-    ProfScope ps(ctx, 0, st);
+    ProfScope ps(ctx, 0, st, k->d);
     TRY(dispatchA(g.N1, a, g.N2, npairs, st));
+    ++ctx->launches;
   }
   if (wantQ) {
     QArgs q{};
@@ -1086,9 +1148,10 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       q.ranks[i] = k->ranks[i];
       q.core_off[i] = k->core_off[i];
     }
-    ProfScope ps(ctx, 3, st);
+    ProfScope ps(ctx, 3, st, k->d);
     qcoef_kernel<<<1, 256, std::max(1, k->C_pad) * sizeof(double), st>>>(q);
     CUDA_TRY(cudaGetLastError());
+    ++ctx->launches;
   }
   if (wantP) {
     PassBArgs b{};
@@ -1114,8 +1177,9 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       b.scratch = ctx->scratch;
     }
     {
-      ProfScope ps(ctx, 1, st);
+      ProfScope ps(ctx, 1, st, k->d);
       TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, st));
+      ++ctx->launches;
     }
     PassCArgs c{};
     c.U = ctx->U;
@@ -1135,8 +1199,9 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       c.res_base[j] = P->res_base[j];
       c.res_cnt[j] = P->res_cnt[j];
     }
-    ProfScope ps(ctx, 2, st);
+    ProfScope ps(ctx, 2, st, k->d);
     TRY(dispatchC(g.N1, c, g.N2, st));
+    ++ctx->launches;
   }
   return TTAGG_OK;
 }
@@ -1457,12 +1522,13 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   const bool host = flags & TTAGG_HOST_PTRS;
   // vec layout: [n natural N][n perm Np][p N][q N][s N]
   const size_t nb = (size_t)g.N * sizeof(double), pb = (size_t)g.Np * sizeof(double);
-  TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, 4 * nb + pb + 1024));
+  const int64_t Na = (g.N + 31) & ~(int64_t)31;  // 256-byte aligned sub-buffers
+  TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, (4 * Na + g.Np) * sizeof(double) + 1024));
   double* v_nat = ctx->vec;
-  double* v_perm = v_nat + g.N;
+  double* v_perm = v_nat + Na;
   double* v_p = v_perm + g.Np;
-  double* v_q = v_p + g.N;
-  double* v_s = v_q + g.N;
+  double* v_q = v_p + Na;
+  double* v_s = v_q + Na;
   const double* nsrc = n;
   if (host) {
     for (int64_t i = 0; i < g.N; ++i)
@@ -1471,6 +1537,7 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
     nsrc = v_nat;
   }
   TRY(launch_permute(nsrc, v_perm, g, 0, st));
+  ++ctx->launches;
   CombineArgs A{};
   TRY(run_orders(ctx, kernels, n_kernels, v_perm, nullptr, 0.0, wantP, wantQ, &A, st));
   A.p = p ? (host ? v_p : p) : nullptr;
@@ -1482,6 +1549,7 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
     dim3 grid(g.N2 / TN2, g.N1 / TN1);
     combine_natural_kernel<<<grid, 256, 0, st>>>(A);
     CUDA_TRY(cudaGetLastError());
+    ++ctx->launches;
   }
   if (host) {
     if (p) CUDA_TRY(cudaMemcpyAsync(p, v_p, nb, cudaMemcpyDeviceToHost, st));
@@ -1507,6 +1575,7 @@ int ttagg_rhs_perm(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_ker
   A.diagp = nullptr;
   ProfScope ps(ctx, 3, st);
   TRY(launch_combine_perm(A, g, st));
+  ++ctx->launches;
   return TTAGG_OK;
 }
 
@@ -1557,9 +1626,10 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   const int64_t nrows = steps / record_every + 1;
   // vec layout: [nat N][A Np][B Np][C Np][rec nrows*4]
   const size_t nb = (size_t)g.N * sizeof(double), pb = (size_t)g.Np * sizeof(double);
-  TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, nb + 3 * pb + (size_t)nrows * 4 * sizeof(double) + 1024));
+  const int64_t Na = (g.N + 31) & ~(int64_t)31;  // 256-byte aligned sub-buffers
+  TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, (Na + 3 * g.Np + nrows * 4) * sizeof(double) + 1024));
   double* v_nat = ctx->vec;
-  double* vA = v_nat + g.N;
+  double* vA = v_nat + Na;
   double* vB = vA + g.Np;
   double* vC = vB + g.Np;
   double* rec = vC + g.Np;
@@ -1697,21 +1767,27 @@ int ttagg_profile_enable(ttagg_ctx* ctx, int on) {
   return TTAGG_OK;
 }
 
-int ttagg_profile_read(ttagg_ctx* ctx, double* out5) {
-  if (!ctx || !out5) return fail(TTAGG_ERR_ARG, "null argument");
+int ttagg_launch_count(ttagg_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return fail(TTAGG_ERR_ARG, "null argument");
+  *out = ctx->launches;
+  return TTAGG_OK;
+}
+
+int ttagg_profile_read(ttagg_ctx* ctx, double* out72) {
+  if (!ctx || !out72) return fail(TTAGG_ERR_ARG, "null argument");
   CUDA_TRY(cudaSetDevice(ctx->device));
-  double acc[5] = {0, 0, 0, 0, 0};
+  for (int i = 0; i < 72; ++i) out72[i] = 0.0;
   for (auto& r : ctx->recs) {
     CUDA_TRY(cudaEventSynchronize(r.b));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
-    acc[r.cls] += ms;
-    if (r.cls == 0 || r.cls == 1 || r.cls == 2) acc[4] += (r.cls == 1) ? 1.0 : 0.0;
+    const int slot = (r.cls * 9 + std::min(std::max(r.d, 0), 8)) * 2;
+    out72[slot] += ms;
+    out72[slot + 1] += 1.0;
     ctx->ev_pool.push_back(r.a);
     ctx->ev_pool.push_back(r.b);
   }
   ctx->recs.clear();
-  for (int i = 0; i < 5; ++i) out5[i] = acc[i];
   return TTAGG_OK;
 }
 
