@@ -1,0 +1,130 @@
+"""Multi-GPU host logic on CPU: rank sharding + all-reduce + replicated RK2
+stage updates (paper_1905_09071_b200.dist), world size 2 over gloo, with the
+oracle standing in for the CUDA engine (test double, never the product)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import rel_inf
+from oracle import rhs_oracle as orc
+from paper_1905_09071_b200.dist import DistRHS, ideal_speedup, rank_counts_of, shard_for_rank
+from paper_1905_09071_b200.parallel import lpt_rank_shards
+from paper_1905_09071_b200.workloads import permutation_power_cp
+
+
+class OracleEngine:
+    """CPU test double of dist.CudaEngine (natural layout torch tensors)."""
+
+    def __init__(self, factors_by_order, shard, n_classes):
+        self.f = factors_by_order
+        self.shard = shard
+        self.n_classes = n_classes
+
+    def vector(self):
+        return torch.zeros(self.n_classes, dtype=torch.float64)
+
+    def to_layout(self, n):
+        return torch.from_numpy(np.array(n, dtype=np.float64))
+
+    def from_layout(self, v):
+        return v.numpy().copy()
+
+    def partial(self, n, k, alpha, out):
+        x = n.numpy() if k is None else (n + alpha * k).numpy()
+        acc = np.zeros(self.n_classes)
+        for d in sorted(self.f):
+            sub = self.shard.get(d, [])
+            if sub:
+                acc += orc.cp_gain(self.f[d], x, ranks=sub)
+                acc += orc.cp_loss(self.f[d], x, ranks=sub)
+        out.copy_(torch.from_numpy(acc))
+
+    def stage(self, base, s, a, out):
+        v = (base + a * s).numpy()
+        k = np.arange(1, v.size + 1, dtype=np.float64)
+        if out is not None:
+            out.copy_(torch.from_numpy(v))
+        return np.array([0.0 if np.all(np.isfinite(v)) else 1.0, v.min(), np.abs(v).max(),
+                         v.sum(), k @ v, (k * k) @ v])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N = 300
+        exps = (0.1, -0.1, 0.05, -0.05, 0.0)
+        f = {d: permutation_power_cp(exps[:d], N) for d in (2, 3, 4, 5)}
+        shard = shard_for_rank(rank_counts_of(f), world, rank)
+        rng = np.random.default_rng(3)
+        n0 = np.exp(-np.arange(1, N + 1) / 40.0) * (1 + 0.05 * rng.random(N))
+        n0 = n0 / n0.sum()
+        drhs = DistRHS(OracleEngine(f, shard, N))
+        s = drhs.rhs(torch.from_numpy(n0.copy()))
+        res = drhs.rk2(n0, 0.0, 0.002, 4, record_every=2)
+        q.put((rank, s.numpy(), res.n, res.rows, res.fail_step, {d: list(v) for d, v in shard.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_sharded_rhs_and_rk2_match_unsharded_oracle():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda x: x[0])
+    N = 300
+    exps = (0.1, -0.1, 0.05, -0.05, 0.0)
+    f = {d: permutation_power_cp(exps[:d], N) for d in (2, 3, 4, 5)}
+    rng = np.random.default_rng(3)
+    n0 = np.exp(-np.arange(1, N + 1) / 40.0) * (1 + 0.05 * rng.random(N))
+    n0 = n0 / n0.sum()
+    ks = {d: {"kind": "cp", "arrays": v} for d, v in f.items()}
+    s_ref = orc.rhs_total(ks, n0)[2]
+    n_ref, _, series = orc.integrate(ks, n0, dt=0.002, steps=4, record_every=2)
+    for rank, s, n, rows, fail, shard in out:
+        assert rel_inf(s, s_ref) <= 1e-12
+        assert rel_inf(n, n_ref) <= 1e-12
+        assert fail == 0
+        np.testing.assert_allclose(np.array(rows), np.array(series.rows()), rtol=1e-11, atol=1e-16)
+    # replicas stay bitwise identical across ranks (same all-reduced sums, same updates)
+    np.testing.assert_array_equal(out[0][2], out[1][2])
+    # the two shards partition every order's rank terms
+    for d in (2, 3, 4, 5):
+        got = sorted(out[0][5].get(d, []) + out[1][5].get(d, []))
+        assert got == list(range(len(f[d][0][0])))
+
+
+def test_lpt_balance_c5():
+    """ideal speedups 2.00 / 3.99 / 7.98 at 2 / 4 / 8 GPUs."""
+    counts = {2: 2, 3: 6, 4: 24, 5: 120}
+    assert ideal_speedup(counts, 1) == pytest.approx(1.0)
+    assert ideal_speedup(counts, 2) >= 1.99
+    assert ideal_speedup(counts, 4) >= 3.98
+    assert ideal_speedup(counts, 8) >= 7.95
+    for world in (1, 2, 3, 4, 8):
+        shards = lpt_rank_shards(counts, world)
+        for d, R in counts.items():
+            owned = sorted(r for s in shards for r in s.get(d, []))
+            assert owned == list(range(R))
+        assert shards == lpt_rank_shards(counts, world)  # deterministic

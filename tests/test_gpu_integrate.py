@@ -1,0 +1,129 @@
+"""GPU RK2 trajectories vs the reference's own (golden) trajectories.
+Tolerance: relative max-norm error <= 1e-8 after the full integration."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1905_09071_b200 as g
+from conftest import assert_rows, rel_inf
+from oracle import rhs_oracle as orc
+from paper_1905_09071_b200.workloads import CONFIGS, initial_state
+
+pytestmark = pytest.mark.gpu
+TRAJ_TOL = 1e-8
+
+
+class Cfg:
+    def __init__(self, n0, dt, steps, record_every, t0=0.0):
+        self.n_classes = n0.size
+        self.initial = g.InitialCondition.from_vector(n0) if n0.min() >= 0 else None
+        self.time = g.TimeGrid(t0, dt, steps)
+        self.record_every = record_every
+
+
+def test_c1_trajectory_vs_reference(golden):
+    c = golden("c1.npz")
+    cfg = CONFIGS["C1"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    final, series = g.integrate(Cfg(initial_state("mono", cfg.n_classes), cfg.dt, cfg.steps, 10), kernels=ks)
+    assert rel_inf(final.n, c["traj_n_final"]) <= TRAJ_TOL
+    assert_rows(series.rows(), c["traj_rows"], TRAJ_TOL)
+    assert not series.negativity_flagged
+
+
+def test_ternary_constant_kernel_vs_reference(golden):
+    t = golden("ternary.npz")
+    ks = g.KernelSet({3: g.constant_tt(1.0, 3, 1024)})
+    final, series = g.integrate(Cfg(initial_state("mono", 1024), 1e-3, 1000, 50), kernels=ks)
+    assert_rows(series.rows(), t["rows"], TRAJ_TOL)
+    assert rel_inf(final.n, t["n_final"]) <= TRAJ_TOL
+    assert abs(series.m0[-1] - (1 + 2 / 3) ** -0.5) < 1e-3
+
+
+def test_c4_shaped_tt_trajectories_vs_reference(golden):
+    c = golden("c4.npz")
+    for n_classes in (128, 256):
+        tag = f"n{n_classes}"
+        ks = g.KernelSet({2: g.TTKernel((c[f"{tag}_d2_c0"], c[f"{tag}_d2_c1"])),
+                          3: g.TTKernel(tuple(c[f"{tag}_d3_c{i}"] for i in range(3)))})
+        final, series = g.integrate(Cfg(initial_state("mono", n_classes), 0.01, 100, 10), kernels=ks)
+        assert rel_inf(final.n, c[f"{tag}_traj_n_final"]) <= TRAJ_TOL
+        assert_rows(series.rows(), c[f"{tag}_traj_rows"], TRAJ_TOL)
+
+
+def test_c3_literal_failure_semantics(golden):
+    """Reference: StepSizeWarning then StepFailureError(step_index=2) with 2 rows."""
+    c = golden("c3.npz")
+    cfg = CONFIGS["C3"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
+        with pytest.raises(g.StepFailureError) as exc:
+            g.integrate(Cfg(initial_state("exp256", cfg.n_classes), cfg.dt, 3, 1), kernels=ks)
+    assert exc.value.step_index == int(c["lit_fail_step"]) == 2
+    assert len(exc.value.series) == len(c["lit_rows"])
+    assert_rows(exc.value.series.rows()[:1], c["lit_rows"][:1], 1e-12)
+    assert_rows(exc.value.series.rows(), c["lit_rows"], 1e-6)  # diverged step-1 row
+    assert any(issubclass(w.category, g.StepSizeWarning) for w in caught) == bool(c["lit_warned"])
+
+
+def test_c3_normalised_trajectory_vs_reference(golden):
+    c = golden("c3.npz")
+    cfg = CONFIGS["C3"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors(1 << 12).items()})
+    final, series = g.integrate(Cfg(initial_state("exp256", 1 << 12, normalised=True), cfg.dt, cfg.steps, 20),
+                                kernels=ks)
+    assert rel_inf(final.n, c["norm4096_n_final"]) <= TRAJ_TOL
+    assert_rows(series.rows(), c["norm4096_rows"], TRAJ_TOL)
+
+
+def test_c5_literal_failure_and_normalised_trajectory(golden):
+    c = golden("c5.npz")
+    cfg = CONFIGS["C5"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors(1 << 12).items()})
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        with pytest.raises(g.StepFailureError) as exc:
+            g.integrate(Cfg(initial_state("c5", 1 << 12), cfg.dt, 3, 1), kernels=ks)
+    assert exc.value.step_index == int(c["lit4096_fail_step"]) == 2
+    assert len(exc.value.series) == len(c["lit4096_rows"])
+    final, series = g.integrate(Cfg(initial_state("c5", 1 << 12, normalised=True), cfg.dt, cfg.steps, 5),
+                                kernels=ks)
+    assert rel_inf(final.n, c["norm4096_n_final"]) <= TRAJ_TOL
+    assert_rows(series.rows(), c["norm4096_rows"], TRAJ_TOL)
+
+
+def test_fused_integrate_matches_stepwise_and_rk2_step():
+    """The device-resident fused loop (ttagg_rk2) == host-orchestrated rk2_step."""
+    cfg = CONFIGS["C5"]
+    N = 1 << 13
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors(N).items()})
+    n0 = initial_state("c5", N, normalised=True)
+    fused_final, fused = g.integrate(Cfg(n0, cfg.dt, 7, 2), kernels=ks)
+    seen = []
+    step_final, stepped = g.integrate(Cfg(n0, cfg.dt, 7, 2), kernels=ks, on_record=lambda s, x: seen.append(s))
+    assert seen == [0, 2, 4, 6]
+    assert rel_inf(fused_final.n, step_final.n) <= 1e-13
+    assert_rows(fused.rows(), stepped.rows(), 1e-12)
+    s = g.ConcentrationState(n0)
+    for _ in range(7):
+        s = g.rk2_step(s, cfg.dt, ks)
+    assert rel_inf(s.n, fused_final.n) <= 1e-13
+    ref_n, _, _ = orc.integrate({d: {"kind": "cp", "arrays": ks[d].factors} for d in ks.orders}, n0,
+                                dt=cfg.dt, steps=7)
+    assert rel_inf(fused_final.n, ref_n) <= 1e-10
+
+
+def test_negativity_flag():
+    """min(n) < -1e-9 max|n| after a step sets the flag and warns once (integrator.py:216-223)."""
+    ks = g.KernelSet({2: g.constant_tt(1.0, 2, 64)})
+    n0 = np.full(64, 1.0)
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
+        _, series = g.integrate(Cfg(n0, 0.9, 3, 1), kernels=ks)
+    ref_n, _, ref = orc.integrate({2: {"kind": "tt", "arrays": ks[2].cores}}, n0, dt=0.9, steps=3)
+    assert series.negativity_flagged == ref.negativity_flagged
+    if ref.negativity_flagged:
+        assert sum(issubclass(w.category, g.StepSizeWarning) for w in caught) == 1

@@ -1,0 +1,279 @@
+"""GPU parity: the sm_100a path through the public API vs the reference's
+own golden vectors, the pinned oracle and FFT-independent properties.
+Tolerance: relative max-norm error <= 1e-10 per RHS (BASELINE north star)."""
+
+import numpy as np
+import pytest
+
+import paper_1905_09071_b200 as g
+from conftest import rel_inf
+from oracle import rhs_oracle as orc
+from paper_1905_09071_b200 import _lib
+from paper_1905_09071_b200.workloads import CONFIGS, initial_state, permutation_power_cp
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def st(n):
+    return g.ConcentrationState(n)
+
+
+def test_extension_is_loaded_and_device_present():
+    ctx = _lib.get_context()
+    assert ctx.handle
+    maps = open("/proc/self/maps").read()
+    assert "libttagg_b200.so" in maps
+
+
+@pytest.mark.parametrize("order", [2, 3, 4, 5])
+def test_cp_random_factors_vs_reference(golden, order):
+    u = golden("unit.npz")
+    k = g.CPKernel(tuple(u[f"cp{order}_f{i}"] for i in range(order)))
+    for s in range(3):
+        n = u[f"cp{order}_n{s}"]
+        assert rel_inf(g.rhs_cp_P(k, st(n)), u[f"cp{order}_P{s}"]) <= TOL
+        assert rel_inf(g.rhs_cp_Q(k, st(n)), u[f"cp{order}_Q{s}"]) <= TOL
+
+
+@pytest.mark.parametrize("tag,order", [("cpodd", 3), ("cptiny", 2)])
+def test_cp_ragged_vs_reference(golden, tag, order):
+    u = golden("unit.npz")
+    k = g.CPKernel(tuple(u[f"{tag}_f{i}"] for i in range(order)))
+    assert rel_inf(g.rhs_cp_P(k, st(u[f"{tag}_n"])), u[f"{tag}_P"]) <= TOL
+    assert rel_inf(g.rhs_cp_Q(k, st(u[f"{tag}_n"])), u[f"{tag}_Q"]) <= TOL
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_tt_brownian_vs_reference(golden, order):
+    u = golden("unit.npz")
+    k = g.TTKernel(tuple(u[f"tt{order}_c{i}"] for i in range(order)))
+    for s in range(3):
+        n = u[f"tt{order}_n{s}"]
+        assert rel_inf(g.rhs_tt_P(k, st(n)), u[f"tt{order}_P{s}"]) <= TOL
+        assert rel_inf(g.rhs_tt_Q(k, st(n)), u[f"tt{order}_Q{s}"]) <= TOL
+
+
+def test_mixed_sets_vs_reference(golden):
+    u = golden("unit.npz")
+    n = u["mix2_n"]
+    ks = g.KernelSet({2: g.CPKernel(permutation_power_cp((0.2, -0.3), n.size)),
+                      3: g.CPKernel(permutation_power_cp((0.3, -0.2, 0.1), n.size))})
+    r = g.rhs_total(ks, st(n))
+    assert rel_inf(r.p, u["mix2_p"]) <= TOL and rel_inf(r.q, u["mix2_q"]) <= TOL
+    assert rel_inf(r.s, u["mix2_s"]) <= TOL
+
+
+def test_known_answers_exact(golden):
+    u = golden("unit.npz")
+    e = np.zeros(8)
+    e[0] = 1.0
+    r = g.rhs_total(g.KernelSet({2: g.constant_tt(1.0, 2, 8)}), st(e))
+    np.testing.assert_allclose(r.s, u["ka_s2"], atol=1e-15)
+    p3 = g.rhs_cp_P(g.constant_cp(1.0, 3, 8), st(e))
+    np.testing.assert_allclose(p3, u["ka_p3"], atol=1e-15)
+    assert np.all(p3[:2] == 0.0)
+    np.testing.assert_allclose(g.rhs_cp_Q(g.constant_cp(1.0, 3, 8), st(e)), u["ka_q3"], atol=1e-15)
+    n = u["conv_n"]
+    np.testing.assert_allclose(g.rhs_tt_P(g.constant_tt(1.75, 3, 16), st(n)), u["conv_P"], rtol=1e-12, atol=1e-15)
+
+
+def test_zero_state_is_exactly_zero():  # test_rhs.py:140-145, 188-193
+    rng = np.random.default_rng(37)
+    k = g.CPKernel(tuple(rng.random((16, 3)) for _ in range(3)))
+    z = st(np.zeros(16))
+    np.testing.assert_array_equal(g.rhs_cp_P(k, z), np.zeros(16))
+    np.testing.assert_array_equal(g.rhs_cp_Q(k, z), np.zeros(16))
+
+
+def test_gain_support_lower_bound_is_exact():  # test_rhs.py:308-317
+    rng = np.random.default_rng(61)
+    for n_classes in (32, 5000, 70000):
+        n = rng.random(n_classes) + 0.5
+        for d in (2, 3, 4, 5):
+            k = g.CPKernel(permutation_power_cp(tuple(rng.uniform(-1, 1, d)), n_classes))
+            p = g.rhs_cp_P(k, st(n))
+            assert np.all(p[: d - 1] == 0.0)
+
+
+@pytest.mark.parametrize("n_classes", [2, 3, 5, 17, 64, 65, 255, 1000, 4097, 12345, 70001])
+def test_ragged_sizes_vs_oracle(n_classes):
+    rng = np.random.default_rng(n_classes)
+    n = rng.random(n_classes)
+    for d in (2, 3, 4, 5, 6):
+        fs = tuple(rng.random((n_classes, 3)) for _ in range(d))
+        k = g.CPKernel(fs)
+        assert rel_inf(g.rhs_cp_P(k, st(n)), orc.cp_gain(fs, n)) <= TOL
+        assert rel_inf(g.rhs_cp_Q(k, st(n)), orc.cp_loss(fs, n)) <= TOL
+
+
+@pytest.mark.parametrize("n_classes,ranks", [(64, (1, 4, 1)), (300, (1, 3, 5, 1)), (4096, (1, 4, 4, 3, 1)),
+                                             (20000, (1, 7, 7, 1)), (65536, (1, 16, 16, 1))])
+def test_tt_random_ranks_vs_oracle(n_classes, ranks):
+    rng = np.random.default_rng(len(ranks) * 7 + n_classes)
+    cores = tuple(rng.random((ranks[l], n_classes, ranks[l + 1])) for l in range(len(ranks) - 1))
+    n = rng.random(n_classes)
+    k = g.TTKernel(cores)
+    assert rel_inf(g.rhs_tt_P(k, st(n)), orc.tt_gain(cores, n)) <= TOL
+    assert rel_inf(g.rhs_tt_Q(k, st(n)), orc.tt_loss(cores, n)) <= TOL
+
+
+def test_c1_vs_reference(golden):
+    c = golden("c1.npz")
+    cfg = CONFIGS["C1"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    r = g.rhs_total(ks, st(initial_state("mono", cfg.n_classes)))
+    assert rel_inf(r.p, c["p0"]) <= TOL and rel_inf(r.q, c["q0"]) <= TOL
+    r = g.rhs_total(ks, st(c["nr"]), breakdown=True)
+    assert rel_inf(r.p, c["pr"]) <= TOL and rel_inf(r.q, c["qr"]) <= TOL
+    for d in cfg.orders:
+        assert rel_inf(r.by_order[d][0], c[f"pr_d{d}"]) <= TOL
+        assert rel_inf(r.by_order[d][1], c[f"qr_d{d}"]) <= TOL
+    np.testing.assert_array_equal(sum(pd for pd, _ in r.by_order.values()), r.p)
+
+
+def test_c2_vs_reference(golden):
+    c = golden("c2.npz")
+    cfg = CONFIGS["C2"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    r = g.rhs_total(ks, st(initial_state("c2", cfg.n_classes)))
+    assert rel_inf(r.p, c["p"]) <= TOL and rel_inf(r.q, c["q"]) <= TOL
+
+
+def _sums(v):
+    k = np.arange(1, v.size + 1, dtype=np.float64)
+    return np.array([v.sum(), k @ v, (k * k) @ v, np.abs(v).sum(), np.abs(v).max()])
+
+
+def test_c3_literal_state_vs_reference(golden):
+    c = golden("c3.npz")
+    cfg = CONFIGS["C3"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    r = g.rhs_total(ks, st(initial_state("exp256", cfg.n_classes)))
+    idx = c["idx"]
+    assert rel_inf(r.p[idx], c["p"]) <= TOL and rel_inf(r.q[idx], c["q"]) <= TOL
+    np.testing.assert_allclose(_sums(r.p), c["p_sums"], rtol=1e-10)
+    np.testing.assert_allclose(_sums(r.q), c["q_sums"], rtol=1e-10)
+
+
+def test_c4_shaped_tt_vs_reference(golden):
+    c = golden("c4.npz")
+    for n_classes in (128, 256):
+        tag = f"n{n_classes}"
+        ks = g.KernelSet({2: g.TTKernel((c[f"{tag}_d2_c0"], c[f"{tag}_d2_c1"])),
+                          3: g.TTKernel(tuple(c[f"{tag}_d3_c{i}"] for i in range(3)))})
+        r = g.rhs_total(ks, st(c[f"{tag}_nr"]))
+        assert rel_inf(r.p, c[f"{tag}_pr"]) <= TOL and rel_inf(r.q, c[f"{tag}_qr"]) <= TOL
+
+
+def test_c5_full_size_vs_reference(golden):
+    """N = 2^20, D = 5, ranks 2/6/24/120 at the literal initial state, against
+    the reference's own rhs_total (TT route on the same tensor) — samples and
+    full-vector moment checksums."""
+    c = golden("c5.npz")
+    cfg = CONFIGS["C5"]
+    N = cfg.n_classes
+    ks = g.KernelSet({d: g.CPKernel(permutation_power_cp(cfg.exponents[:d], N)) for d in cfg.orders})
+    r = g.rhs_total(ks, st(initial_state("c5", N)), breakdown=True)
+    idx = c["idx"]
+    assert rel_inf(r.p[idx], c["p"]) <= TOL and rel_inf(r.q[idx], c["q"]) <= TOL
+    for d in cfg.orders:
+        assert rel_inf(r.by_order[d][0][idx], c[f"p_d{d}"]) <= TOL
+        assert rel_inf(r.by_order[d][1][idx], c[f"q_d{d}"]) <= TOL
+    np.testing.assert_allclose(_sums(r.p)[[0, 1, 3, 4]], c["p_sums"][[0, 1, 3, 4]], rtol=1e-10)
+    np.testing.assert_allclose(_sums(r.q), c["q_sums"], rtol=1e-10)
+    # the fused all-orders path agrees with the per-order path
+    r2 = g.rhs_total(ks, st(initial_state("c5", N)))
+    assert rel_inf(r2.s, r.s) <= 1e-14
+
+
+def test_c5_full_size_closed_form_every_order():
+    """FFT-length-independent property at full size: the permutation-power
+    gain equals the collapsed d-fold convolution."""
+    cfg = CONFIGS["C5"]
+    N = cfg.n_classes
+    n = initial_state("c5", N)
+    sizes = np.arange(1, N + 1, dtype=np.float64)
+    for d in cfg.orders:
+        p = g.rhs_cp_P(g.CPKernel(permutation_power_cp(cfg.exponents[:d], N)), st(n))
+        L = 1 << int(np.ceil(np.log2(d * N + 1)))
+        spec = np.ones(L // 2 + 1, dtype=complex)
+        for j in range(d):
+            v = np.zeros(L)
+            v[1 : N + 1] = np.exp(cfg.exponents[j] * np.log(sizes)) * n
+            spec *= np.fft.rfft(v)
+        conv = np.fft.irfft(spec, n=L)
+        ref = np.zeros(N)
+        ref[d - 1 :] = conv[d : N + 1]
+        assert rel_inf(p, ref) <= TOL
+
+
+def test_mass_conservation_before_boundary_contact():  # test_rhs.py:276-292
+    rng = np.random.default_rng(53)
+    for n_classes in (64, 1024, 1 << 16):
+        n = np.zeros(n_classes)
+        n[: n_classes // 4] = rng.random(n_classes // 4)
+        sizes = np.arange(1, n_classes + 1, dtype=np.float64)
+        for k in (g.constant_tt(1.0, 3, n_classes),
+                  g.CPKernel(permutation_power_cp((1 / 3, -1 / 3, 0.0), n_classes))):
+            r = g.rhs_total(g.KernelSet({3: k}) if n_classes > 64 else {3: k}, st(n))
+            assert abs(sizes @ r.s) <= 1e-12 * (sizes @ r.p)
+
+
+def test_order_power_scaling():  # test_rhs.py:295-305
+    rng = np.random.default_rng(59)
+    n = rng.random(3000)
+    for d in (2, 3, 4):
+        k = g.CPKernel(permutation_power_cp(tuple(rng.uniform(-1, 1, d)), 3000))
+        base = g.rhs_total({d: k}, st(n))
+        scaled = g.rhs_total({d: k}, st(1.7 * n))
+        np.testing.assert_allclose(scaled.p, 1.7**d * base.p, rtol=1e-12, atol=1e-12 * np.abs(scaled.p).max())
+        np.testing.assert_allclose(scaled.q, 1.7**d * base.q, rtol=1e-12)
+
+
+def test_bitwise_determinism():  # test_rhs.py:320-327
+    cfg = CONFIGS["C3"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors(1 << 16).items()})
+    n = initial_state("exp256", 1 << 16)
+    a = g.rhs_total(ks, st(n)).s
+    b = g.rhs_total(ks, st(n)).s
+    np.testing.assert_array_equal(a, b)
+
+
+def test_rank_shards_sum_to_full_rhs():
+    """Multi-GPU premise on one GPU: partial RHS over LPT rank shards (each its
+    own upload and launch) sum to the unsharded RHS."""
+    import torch
+
+    cfg = CONFIGS["C5"]
+    N = 1 << 14
+    f = {d: permutation_power_cp(cfg.exponents[:d], N) for d in cfg.orders}
+    n = initial_state("c5", N)
+    ctx = _lib.get_context()
+    full = g.rhs_total(g.KernelSet({d: g.CPKernel(v) for d, v in f.items()}), st(n)).s
+    Np, _, _ = _lib.geometry(N)
+    dev = torch.device("cuda", ctx.device)
+    nt = torch.from_numpy(n).to(dev)
+    nperm = torch.zeros(Np, dtype=torch.float64, device=dev)
+    ctx.permute(N, nt.data_ptr(), nperm.data_ptr(), 0, None)
+    for world in (2, 4, 8):
+        acc = torch.zeros(Np, dtype=torch.float64, device=dev)
+        for shard in g.lpt_rank_shards({d: v[0].shape[1] for d, v in f.items()}, world):
+            dks = [ctx.upload_cp(f[d], rank_subset=shard[d]) for d in sorted(shard)]
+            part = torch.zeros(Np, dtype=torch.float64, device=dev)
+            ctx.rhs_perm(dks, nperm.data_ptr(), None, 0.0, part.data_ptr(), None)
+            acc += part
+        out = torch.empty(N, dtype=torch.float64, device=dev)
+        ctx.permute(N, acc.data_ptr(), out.data_ptr(), 1, None)
+        torch.cuda.synchronize()
+        assert rel_inf(out.cpu().numpy(), full) <= 1e-13
+
+
+def test_error_behaviour():
+    with pytest.raises(g.KernelError):
+        g.rhs_total(g.KernelSet({2: g.constant_tt(1.0, 2, 8)}), st(np.ones(9)))
+    with pytest.raises(ValueError):
+        g.ConcentrationState(np.array([1.0, np.nan]))
+    with pytest.raises(_lib.TTaggError, match="exceeds"):
+        g.rhs_cp_P(g.CPKernel((np.ones(((1 << 20) + 1, 1)), np.ones(((1 << 20) + 1, 1)))),
+                   st(np.ones((1 << 20) + 1)))
