@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -218,6 +219,7 @@ struct PassAArgs {
   const double2* tabLhi;
   int d, N2, K_rows, nblk, want_T;
   int res_base[MAXRES], res_cnt[MAXRES];
+  int dbg;  // debug: 1 skip stores, 2 skip FFTs, 4 skip input loads
 };
 
 // One CTA = one column pair x G adjacent columns n2, run by two thread
@@ -378,6 +380,193 @@ __global__ void __launch_bounds__(512, 1) passA_kernel(const PassAArgs a) {
         }
       }
     }
+  }
+}
+
+// ---- bulk-async (TMA) helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Persistent pass A for column transforms of >= 32 threads (N1 >= 512): one
+// work item = (column pair, n2).  Two thread groups transform residues j and
+// d-j concurrently and separate the two real columns through the Hermitian
+// mirror (one CTA barrier per round besides the FFT's group barriers); the
+// next item's inputs are prefetched into L2 at the start of each item.
+template <int N1>
+__global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassAArgs a, int nitems) {
+  constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1), H = N1 / 2;
+  constexpr int NW = 2 * T / 32;
+  static_assert(T >= 32, "warp-multiple groups");
+  extern __shared__ double2 smem[];
+  __shared__ double red[2][NW];
+  __shared__ double2 Pst[16];
+  __shared__ double2 Kst[MAXRES * 2][16];  // W_K^(j T r): twist steps per residue
+  const int tid = threadIdx.x, grp = tid >= T ? 1 : 0, t = tid - grp * T;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int d = a.d;
+  const int N2 = a.N2;
+  double2* zbuf = smem;
+  double2* buf0 = smem + N1;
+  double2* buf1 = buf0 + SE;
+  double2* mybuf = grp ? buf1 : buf0;
+  double2* otbuf = grp ? buf0 : buf1;
+  const size_t Np = (size_t)N1 * N2;
+  const size_t colT = (size_t)a.K_rows * N2;
+  const GroupSync gs{1 + grp, T};
+  for (int i = tid; i < d * 16; i += blockDim.x) {
+    const int j = i / 16, r = i % 16;
+    const cplx w = ld_c(a.tabK + (j * T * r) % (d * N1));
+    Kst[j][r] = make_double2(w.x, w.y);
+  }
+  // twist base W_K^(j t) of this thread for residue j (one table load)
+  auto twist_base = [&](int j) { return ld_c(a.tabK + j * t); };
+
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int pair = item / N2, n2 = item - pair * N2;
+    const size_t e0 = (size_t)n2 * N1;
+    const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
+    const double* xb = xa + Np;
+    if (tid == 0) {
+      const int nx = item + gridDim.x;
+      if (nx < nitems) {
+        const int np_ = nx / N2, nn2 = nx - np_ * N2;
+        const double* nxa = a.X + (size_t)(2 * np_) * Np + (size_t)nn2 * N1;
+        prefetch_l2(nxa, N1 * 8);
+        prefetch_l2(nxa + Np, N1 * 8);
+        prefetch_l2(a.nv + (size_t)nn2 * N1, N1 * 8);
+        if (a.kv) prefetch_l2(a.kv + (size_t)nn2 * N1, N1 * 8);
+      }
+    }
+    // stage z = (a + i b) * n and reduce the column sums (shuffles + one barrier)
+    {
+      const double2* xa2 = reinterpret_cast<const double2*>(xa);
+      const double2* xb2 = reinterpret_cast<const double2*>(xb);
+      const double2* nv2 = reinterpret_cast<const double2*>(a.nv + e0);
+      const double2* kv2 = a.kv ? reinterpret_cast<const double2*>(a.kv + e0) : nullptr;
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int q = 0; q < N1 / 4 / T; ++q) {
+        const int i = tid + 2 * T * q;
+        double2 w = make_double2(1.0, 1.0), ua = make_double2(i, 1.0), ub = make_double2(1.0, i);
+        if (!(a.dbg & 4)) {
+          w = __ldg(nv2 + i);
+          if (kv2) {
+            const double2 k = __ldg(kv2 + i);
+            w.x = __dadd_rn(w.x, __dmul_rn(a.alpha, k.x));
+            w.y = __dadd_rn(w.y, __dmul_rn(a.alpha, k.y));
+          }
+          ua = __ldg(xa2 + i);
+          ub = __ldg(xb2 + i);
+        }
+        const double va0 = ua.x * w.x, va1 = ua.y * w.y, vb0 = ub.x * w.x, vb1 = ub.y * w.y;
+        zbuf[2 * i] = make_double2(va0, vb0);
+        zbuf[2 * i + 1] = make_double2(va1, vb1);
+        sa += va0 + va1;
+        sb += vb0 + vb1;
+      }
+      sa = warp_sum(sa);
+      sb = warp_sum(sb);
+      if (lane == 0) {
+        red[0][wid] = sa;
+        red[1][wid] = sb;
+      }
+      if (tid < 16) {
+        const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * tid);
+        Pst[tid] = make_double2(w.x, w.y);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double ta = 0.0, tb = 0.0;
+        for (int w = 0; w < NW; ++w) {
+          ta += red[0][w];
+          tb += red[1][w];
+        }
+        a.dots[(size_t)(2 * pair) * a.nblk + n2] = ta;
+        a.dots[(size_t)(2 * pair + 1) * a.nblk + n2] = tb;
+      }
+    }
+    double2* Ta = a.T + (size_t)(2 * pair) * colT + (size_t)n2 * a.K_rows;
+    double2* Tb = Ta + colT;
+    auto emit = [&](int rho, cplx Z, cplx Zm, cplx w) {
+      const cplx cz = cconj(Zm);
+      const cplx A = cscale(cadd(Z, cz), 0.5);
+      const cplx B = cscale(mul_mi(csub(Z, cz)), 0.5);
+      if (!(a.dbg & 1)) {
+        sts_c(Ta + rho, cmul(A, w));
+        sts_c(Tb + rho, cmul(B, w));
+      }
+    };
+
+    // residue pairs (j, d-j), 0 < j < d/2
+    for (int j = 1; 2 * j < d; ++j) {
+      const int jr = grp ? d - j : j;
+      cplx v[E];
+      {
+        const cplx tb = twist_base(jr);
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+          v[r] = cmul(lds_c(zbuf + t + T * r), cmul(tb, lds_c(&Kst[jr][r])));
+      }
+      if (!(a.dbg & 2)) fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
+#pragma unroll
+      for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
+      __syncthreads();
+      // group 0: rows k1 = t + T r (< H); group 1: rows k1 = N1-1-(t + T r) (>= H)
+      const int kb = grp ? j + d * (N1 - 1 - t) : j + d * t;
+      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kb);
+      const int rho0 = a.res_base[j];
+#pragma unroll
+      for (int r = 0; r < E / 2; ++r) {
+        const int kk = t + T * r;
+        const cplx o = lds_c(otbuf + pad16(N1 - 1 - kk));
+        if (grp == 0) {
+          emit(rho0 + kk, v[r], o, cmul(b, lds_c(Pst + r)));
+        } else {
+          emit(rho0 + N1 - 1 - kk, o, v[r], cmulc(b, lds_c(Pst + r)));
+        }
+      }
+      __syncthreads();  // buffers are rewritten by the next round's FFTs
+    }
+    // self-mirrored residues: 0 on group 0 (rows k1 <= H), d/2 (even d) on group 1 (rows k1 < H)
+    {
+      const int jr = grp == 0 ? 0 : ((d & 1) ? -1 : d / 2);
+      if (jr >= 0) {
+        cplx v[E];
+        const cplx tb = twist_base(jr);
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const cplx z = lds_c(zbuf + t + T * r);
+          v[r] = jr == 0 ? z : cmul(z, cmul(tb, lds_c(&Kst[jr][r])));
+        }
+        if (!(a.dbg & 2)) fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
+#pragma unroll
+        for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
+        gs();
+        const int cnt = jr == 0 ? H + 1 : H;
+        const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * (jr + d * t));
+        const int rho0 = a.res_base[jr];
+#pragma unroll
+        for (int r = 0; r <= E / 2; ++r) {
+          const int k1 = t + T * r;
+          if (k1 < cnt) {
+            const int mk = jr == 0 ? ((N1 - k1) & (N1 - 1)) : (N1 - 1 - k1);
+            emit(rho0 + k1, v[r], lds_c(mybuf + pad16(mk)), cmul(b, lds_c(Pst + (r & 15))));
+          }
+        }
+      }
+    }
+    __syncthreads();  // zbuf and the buffers are rewritten by the next item
   }
 }
 
@@ -979,6 +1168,23 @@ constexpr int passA_G(int T, int N2) { return std::max(1, std::min(128 / T, N2))
 template <int N1>
 int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   constexpr int T = fft_t(N1);
+  if constexpr (T >= 32) {
+    static int nsm = 0, occ = 0;
+    const size_t smem = ((size_t)N1 + 2 * (size_t)fft_smem_elems(N1)) * sizeof(double2);
+    TRY(set_smem(passA_tma_kernel<N1>, smem));
+    if (!nsm) {
+      int dev = 0;
+      CUDA_TRY(cudaGetDevice(&dev));
+      CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passA_tma_kernel<N1>, 2 * T, smem));
+      occ = std::max(occ, 1);
+    }
+    const int nitems = npairs * N2;
+    const int grid = std::min(nitems, nsm * occ);
+    passA_tma_kernel<N1><<<grid, 2 * T, smem, st>>>(a, nitems);
+    CUDA_TRY(cudaGetLastError());
+    return TTAGG_OK;
+  }
   const int G = passA_G(T, N2);
   const size_t smem = ((size_t)G * N1 + (size_t)2 * G * fft_smem_elems(N1)) * sizeof(double2);
   TRY(set_smem(passA_kernel<N1>, smem));
@@ -988,7 +1194,7 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   return TTAGG_OK;
 }
 
-int nblk_for(int N1, int N2) { return N2 / passA_G(fft_t(N1), N2); }
+int nblk_for(int N1, int N2) { return fft_t(N1) >= 32 ? N2 : N2 / passA_G(fft_t(N1), N2); }
 
 int dispatchA(int N1, const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   switch (N1) {
@@ -1126,6 +1332,14 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
   a.K_rows = P->K_rows;
   a.nblk = k->nblk;
   a.want_T = wantP ? 1 : 0;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("TTAGG_DEBUG_PASSA");
+      dbg = e ? atoi(e) : 0;
+    }
+    a.dbg = dbg;
+  }
   for (int j = 0; j < MAXRES; ++j) {
     a.res_base[j] = P->res_base[j];
     a.res_cnt[j] = P->res_cnt[j];
