@@ -383,17 +383,7 @@ __global__ void __launch_bounds__(512, 1) passA_kernel(const PassAArgs a) {
   }
 }
 
-// ---- bulk-async (TMA) helpers
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// ---- L2 prefetch (bulk-async engine)
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -432,13 +422,61 @@ __global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassA
   // twist base W_K^(j t) of this thread for residue j (one table load)
   auto twist_base = [&](int j) { return ld_c(a.tabK + j * t); };
 
+  // stage z = (a + i b) * n of `it` into zbuf with threads [first, first+nthr)
+  // and reduce its two column sums (warp shuffles, one barrier `bar`)
+  auto stage = [&](int it, int first, int nthr, auto&& bar) {
+    const int pp = it / N2, nn = it - pp * N2;
+    const size_t e = (size_t)nn * N1;
+    const double2* xa2 = reinterpret_cast<const double2*>(a.X + (size_t)(2 * pp) * Np + e);
+    const double2* xb2 = reinterpret_cast<const double2*>(a.X + (size_t)(2 * pp + 1) * Np + e);
+    const double2* nv2 = reinterpret_cast<const double2*>(a.nv + e);
+    const double2* kv2 = a.kv ? reinterpret_cast<const double2*>(a.kv + e) : nullptr;
+    const int me = tid - first;
+    double sa = 0.0, sb = 0.0;
+#pragma unroll 4
+    for (int i = me; i < N1 / 2; i += nthr) {
+      double2 w = make_double2(1.0, 1.0), ua = make_double2(i, 1.0), ub = make_double2(1.0, i);
+      if (!(a.dbg & 4)) {
+        w = __ldg(nv2 + i);
+        if (kv2) {
+          const double2 k = __ldg(kv2 + i);
+          w.x = __dadd_rn(w.x, __dmul_rn(a.alpha, k.x));
+          w.y = __dadd_rn(w.y, __dmul_rn(a.alpha, k.y));
+        }
+        ua = __ldg(xa2 + i);
+        ub = __ldg(xb2 + i);
+      }
+      const double va0 = ua.x * w.x, va1 = ua.y * w.y, vb0 = ub.x * w.x, vb1 = ub.y * w.y;
+      zbuf[2 * i] = make_double2(va0, vb0);
+      zbuf[2 * i + 1] = make_double2(va1, vb1);
+      sa += va0 + va1;
+      sb += vb0 + vb1;
+    }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) {
+      red[0][wid] = sa;
+      red[1][wid] = sb;
+    }
+    bar();
+    if (me == 0) {
+      double ta = 0.0, tb = 0.0;
+      for (int w = first / 32; w < (first + nthr) / 32; ++w) {
+        ta += red[0][w];
+        tb += red[1][w];
+      }
+      a.dots[(size_t)(2 * pp) * a.nblk + nn] = ta;
+      a.dots[(size_t)(2 * pp + 1) * a.nblk + nn] = tb;
+    }
+  };
+  auto cta_bar = [&]() { __syncthreads(); };
+  bool staged = false;  // zbuf already holds this item's z (staged during the previous item)
+
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int pair = item / N2, n2 = item - pair * N2;
-    const size_t e0 = (size_t)n2 * N1;
-    const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
-    const double* xb = xa + Np;
+    const int next = item + gridDim.x;
     if (tid == 0) {
-      const int nx = item + gridDim.x;
+      const int nx = staged ? next : item + gridDim.x;
       if (nx < nitems) {
         const int np_ = nx / N2, nn2 = nx - np_ * N2;
         const double* nxa = a.X + (size_t)(2 * np_) * Np + (size_t)nn2 * N1;
@@ -448,54 +486,12 @@ __global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassA
         if (a.kv) prefetch_l2(a.kv + (size_t)nn2 * N1, N1 * 8);
       }
     }
-    // stage z = (a + i b) * n and reduce the column sums (shuffles + one barrier)
-    {
-      const double2* xa2 = reinterpret_cast<const double2*>(xa);
-      const double2* xb2 = reinterpret_cast<const double2*>(xb);
-      const double2* nv2 = reinterpret_cast<const double2*>(a.nv + e0);
-      const double2* kv2 = a.kv ? reinterpret_cast<const double2*>(a.kv + e0) : nullptr;
-      double sa = 0.0, sb = 0.0;
-#pragma unroll
-      for (int q = 0; q < N1 / 4 / T; ++q) {
-        const int i = tid + 2 * T * q;
-        double2 w = make_double2(1.0, 1.0), ua = make_double2(i, 1.0), ub = make_double2(1.0, i);
-        if (!(a.dbg & 4)) {
-          w = __ldg(nv2 + i);
-          if (kv2) {
-            const double2 k = __ldg(kv2 + i);
-            w.x = __dadd_rn(w.x, __dmul_rn(a.alpha, k.x));
-            w.y = __dadd_rn(w.y, __dmul_rn(a.alpha, k.y));
-          }
-          ua = __ldg(xa2 + i);
-          ub = __ldg(xb2 + i);
-        }
-        const double va0 = ua.x * w.x, va1 = ua.y * w.y, vb0 = ub.x * w.x, vb1 = ub.y * w.y;
-        zbuf[2 * i] = make_double2(va0, vb0);
-        zbuf[2 * i + 1] = make_double2(va1, vb1);
-        sa += va0 + va1;
-        sb += vb0 + vb1;
-      }
-      sa = warp_sum(sa);
-      sb = warp_sum(sb);
-      if (lane == 0) {
-        red[0][wid] = sa;
-        red[1][wid] = sb;
-      }
-      if (tid < 16) {
-        const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * tid);
-        Pst[tid] = make_double2(w.x, w.y);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double ta = 0.0, tb = 0.0;
-        for (int w = 0; w < NW; ++w) {
-          ta += red[0][w];
-          tb += red[1][w];
-        }
-        a.dots[(size_t)(2 * pair) * a.nblk + n2] = ta;
-        a.dots[(size_t)(2 * pair + 1) * a.nblk + n2] = tb;
-      }
+    if (!staged) stage(item, 0, 2 * T, cta_bar);
+    if (tid < 16) {
+      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * tid);
+      Pst[tid] = make_double2(w.x, w.y);
     }
+    __syncthreads();
     double2* Ta = a.T + (size_t)(2 * pair) * colT + (size_t)n2 * a.K_rows;
     double2* Tb = Ta + colT;
     auto emit = [&](int rho, cplx Z, cplx Zm, cplx w) {
@@ -538,9 +534,15 @@ __global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassA
       }
       __syncthreads();  // buffers are rewritten by the next round's FFTs
     }
-    // self-mirrored residues: 0 on group 0 (rows k1 <= H), d/2 (even d) on group 1 (rows k1 < H)
+    // self-mirrored residues: 0 on group 0 (rows k1 <= H), d/2 (even d) on group 1 (rows k1 < H);
+    // for odd d group 1 is free and stages the next item once group 0 has read zbuf
+    const bool overlap = (d & 1) && next < nitems;
     {
       const int jr = grp == 0 ? 0 : ((d & 1) ? -1 : d / 2);
+      if (grp == 1 && overlap) {
+        asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");  // group 0 has its z in registers
+        stage(next, T, T, gs);
+      }
       if (jr >= 0) {
         cplx v[E];
         const cplx tb = twist_base(jr);
@@ -549,6 +551,7 @@ __global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassA
           const cplx z = lds_c(zbuf + t + T * r);
           v[r] = jr == 0 ? z : cmul(z, cmul(tb, lds_c(&Kst[jr][r])));
         }
+        if (grp == 0 && overlap) asm volatile("bar.arrive 3, %0;" ::"r"(2 * T) : "memory");
         if (!(a.dbg & 2)) fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
 #pragma unroll
         for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
@@ -567,6 +570,7 @@ __global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassA
       }
     }
     __syncthreads();  // zbuf and the buffers are rewritten by the next item
+    staged = overlap;
   }
 }
 
@@ -585,14 +589,6 @@ struct PassBArgs {
   int d, K, K_rows, C, kind, Rmax;
   int ranks[MAXD + 1];
 };
-
-__device__ __forceinline__ void cp_async16(double2* sdst, const double2* gsrc) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int NLEFT>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NLEFT) : "memory"); }
 
 // One CTA = 8 exchange rows x T threads per row (128 threads).  Lanes run
 // over the 8 rows fastest so every warp load reads whole 128-byte segments
