@@ -835,8 +835,20 @@ __device__ __forceinline__ void pq_at(const CombineArgs& A, size_t e, double nvv
     const CombineOrder& o = A.o[k];
     if (o.p) P += __ldg(o.p + e);
     if (o.coef) {
+      // loads batched 8 at a time, summed in rank order (deterministic)
       double tail = 0.0;
-      for (int r = 0; r < o.ntail; ++r) tail += __ldg(o.X + (size_t)__ldg(o.tail + r) * Np + e) * __ldg(o.coef + r);
+      for (int r0 = 0; r0 < o.ntail; r0 += 8) {
+        double xv[8], cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = r0 + u;
+          xv[u] = r < o.ntail ? __ldg(o.X + (size_t)__ldg(o.tail + r) * Np + e) : 0.0;
+          cv[u] = r < o.ntail ? __ldg(o.coef + r) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (r0 + u < o.ntail) tail += xv[u] * cv[u];
+      }
       Q += -(nvv * tail) / o.qdiv;
     }
   }
@@ -1731,7 +1743,7 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   if (!wantP && !wantQ) wantP = wantQ = true;
   const bool host = flags & TTAGG_HOST_PTRS;
   // vec layout: [n natural N][n perm Np][p N][q N][s N]
-  const size_t nb = (size_t)g.N * sizeof(double), pb = (size_t)g.Np * sizeof(double);
+  const size_t nb = (size_t)g.N * sizeof(double);
   const int64_t Na = (g.N + 31) & ~(int64_t)31;  // 256-byte aligned sub-buffers
   TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, (4 * Na + g.Np) * sizeof(double) + 1024));
   double* v_nat = ctx->vec;
@@ -1835,7 +1847,7 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   const bool host = flags & TTAGG_HOST_PTRS;
   const int64_t nrows = steps / record_every + 1;
   // vec layout: [nat N][A Np][B Np][C Np][rec nrows*4]
-  const size_t nb = (size_t)g.N * sizeof(double), pb = (size_t)g.Np * sizeof(double);
+  const size_t nb = (size_t)g.N * sizeof(double);
   const int64_t Na = (g.N + 31) & ~(int64_t)31;  // 256-byte aligned sub-buffers
   TRY(ensure((void**)&ctx->vec, &ctx->vec_bytes, (Na + 3 * g.Np + nrows * 4) * sizeof(double) + 1024));
   double* v_nat = ctx->vec;
