@@ -1042,7 +1042,7 @@ __global__ void rk2_book_init_kernel(const double* diag0, int64_t* book, double*
 // ---------------------------------------------------------------------------
 // dir 0: natural (length N) -> perm (length Np, zero padded); dir 1: perm -> natural
 __global__ void permute_kernel(const double* __restrict__ in, double* __restrict__ out, long long N, int N1, int N2,
-                               int dir) {
+                               int dir, int* nonfinite = nullptr) {
   __shared__ double tile[32][33];
   const int TN1 = min(32, N1), TN2 = min(32, N2);
   const int n1_0 = blockIdx.y * TN1, n2_0 = blockIdx.x * TN2;
@@ -1051,7 +1051,9 @@ __global__ void permute_kernel(const double* __restrict__ in, double* __restrict
     for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
       const int i2 = idx % TN2, i1 = idx / TN2;
       const long long o = (long long)(n1_0 + i1) * N2 + (n2_0 + i2);
-      tile[i2][i1] = o < N ? in[o] : 0.0;
+      const double x = o < N ? in[o] : 0.0;
+      if (nonfinite && !isfinite(x)) *nonfinite = 1;  // benign race: every writer stores 1
+      tile[i2][i1] = x;
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < TN1 * TN2; idx += blockDim.x) {
@@ -1468,10 +1470,10 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
   return TTAGG_OK;
 }
 
-int launch_permute(const double* in, double* out, const Geom& g, int dir, cudaStream_t st) {
+int launch_permute(const double* in, double* out, const Geom& g, int dir, cudaStream_t st, int* nonfinite = nullptr) {
   const int TN1 = std::min(32, g.N1), TN2 = std::min(32, g.N2);
   dim3 grid(g.N2 / TN2, g.N1 / TN1);
-  permute_kernel<<<grid, 256, 0, st>>>(in, out, g.N, g.N1, g.N2, dir);
+  permute_kernel<<<grid, 256, 0, st>>>(in, out, g.N, g.N1, g.N2, dir, nonfinite);
   CUDA_TRY(cudaGetLastError());
   return TTAGG_OK;
 }
@@ -1752,13 +1754,13 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   double* v_q = v_p + Na;
   double* v_s = v_q + Na;
   const double* nsrc = n;
+  int* dflag = reinterpret_cast<int*>(ctx->book + 6);
   if (host) {
-    for (int64_t i = 0; i < g.N; ++i)
-      if (!std::isfinite(n[i])) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
+    CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), st));
     CUDA_TRY(cudaMemcpyAsync(v_nat, n, nb, cudaMemcpyHostToDevice, st));
     nsrc = v_nat;
   }
-  TRY(launch_permute(nsrc, v_perm, g, 0, st));
+  TRY(launch_permute(nsrc, v_perm, g, 0, st, host ? dflag : nullptr));
   ++ctx->launches;
   CombineArgs A{};
   TRY(run_orders(ctx, kernels, n_kernels, v_perm, nullptr, 0.0, wantP, wantQ, &A, st));
@@ -1774,10 +1776,13 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
     ++ctx->launches;
   }
   if (host) {
+    int hflag = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (p) CUDA_TRY(cudaMemcpyAsync(p, v_p, nb, cudaMemcpyDeviceToHost, st));
     if (q) CUDA_TRY(cudaMemcpyAsync(q, v_q, nb, cudaMemcpyDeviceToHost, st));
     if (s) CUDA_TRY(cudaMemcpyAsync(s, v_s, nb, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (hflag) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
   }
   return TTAGG_OK;
 }

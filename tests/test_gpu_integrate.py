@@ -127,3 +127,22 @@ def test_negativity_flag():
     assert series.negativity_flagged == ref.negativity_flagged
     if ref.negativity_flagged:
         assert sum(issubclass(w.category, g.StepSizeWarning) for w in caught) == 1
+
+
+def test_dist_engine_rk2_matches_fused_integrate():
+    """The multi-GPU orchestration (dist.DistRHS + CudaEngine: perm-layout
+    partial RHS, all-reduce, ttagg_stage updates) on one GPU == ttagg_rk2."""
+    from paper_1905_09071_b200.dist import CudaEngine, DistRHS, shard_for_rank
+    from paper_1905_09071_b200 import _lib
+
+    cfg = CONFIGS["C5"]
+    N = 1 << 13
+    f = cfg.cp_factors(N)
+    n0 = initial_state("c5", N, normalised=True)
+    eng = CudaEngine(f, shard_for_rank({d: v[0].shape[1] for d, v in f.items()}, 1, 0), N, _lib.get_context().device)
+    res = DistRHS(eng).rk2(n0, 0.0, cfg.dt, 6, record_every=2)
+    ks = g.KernelSet({d: g.CPKernel(v) for d, v in f.items()})
+    final, series = g.integrate(Cfg(n0, cfg.dt, 6, 2), kernels=ks)
+    assert res.fail_step == 0
+    assert rel_inf(res.n, final.n) <= 1e-13
+    assert_rows(res.rows, series.rows(), 1e-12)

@@ -274,6 +274,14 @@ def test_error_behaviour():
         g.rhs_total(g.KernelSet({2: g.constant_tt(1.0, 2, 8)}), st(np.ones(9)))
     with pytest.raises(ValueError):
         g.ConcentrationState(np.array([1.0, np.nan]))
+    # the C-ABI checks host inputs on the device (TTAGG_ERR_NONFINITE -> ValueError)
+    ctx = _lib.get_context()
+    dk = ctx.device_kernel(g.constant_tt(1.0, 2, 8))
+    bad = np.ones(8)
+    bad[3] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        ctx.rhs_host([dk], bad)
+    np.testing.assert_allclose(ctx.rhs_host([dk], np.ones(8))["s"][:2], [-8.0, -7.5])
     with pytest.raises(_lib.TTaggError, match="exceeds"):
         g.rhs_cp_P(g.CPKernel((np.ones(((1 << 20) + 1, 1)), np.ones(((1 << 20) + 1, 1)))),
                    st(np.ones((1 << 20) + 1)))
