@@ -365,9 +365,19 @@ def main():
         per_ms = tot_ms / cnt
         bytes_launch = (model["passA"] if cls == 0 else model["passB"])[d]
         achieved = bytes_launch / (per_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"pass{'AB'[cls]} d={d}", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                "launch_ms": per_ms, "bytes_per_launch": bytes_launch}
+        kname = f"pass{'AB'[cls]} d={d}"
+        traffic = None
+        try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")) as fh:
+                tk = json.load(fh)["kernels"].get(kname)
+            if tk and N == 1 << 20:
+                traffic = tk["dram_bytes"]
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "launch_ms": per_ms, "bytes_per_launch": bytes_launch,
+                "traffic_source": "profiles/r01_roofline_traffic.json (ncu dram__bytes_read+write per launch)"}
     rhs_gbs = model["B_RHS"] / (ms_step * 1e-3) / 1e9
     breakdown = {f"{'ABCO'[c]}{d}": round(v[0] / args.steps, 4) for (c, d), v in sorted(prof.items())}
 
