@@ -50,7 +50,7 @@ using namespace ttagg;
 namespace {
 
 constexpr int MAXD = 8;
-constexpr int MAXRES = MAXD / 2 + 1;
+constexpr int MAXRES = MAXD;  // one residue class per order
 constexpr int MAXORD = 8;
 constexpr int LSPLIT = 11;
 constexpr int LLO = 1 << LSPLIT;
@@ -222,59 +222,67 @@ struct PassAArgs {
   int dbg;  // debug: 1 skip stores, 2 skip FFTs, 4 skip input loads
 };
 
-// One CTA = one column pair x G adjacent columns n2, run by two thread
-// groups of T*G threads (two residue FFTs in flight, named barriers); the
-// weighted input z = (a + i b) * n is staged once in shared memory.
+// Emit one column-transform output of the packed pair z = a + i b
+// (Y = Zcol[kappa], kappa = j + d k1, w = W_L^(n2 kappa)) into the exchange:
+//   P plane, row kappa (kappa <= K/2):      Y w
+//   M plane, row kappa' = K - kappa (kappa >= K/2, or kappa = 0):
+//       conj(Y w) W_L^(n2 K)  (= conj(Zcol[K-kappa']) W_L^(n2 kappa'); kappa = 0: conj(Y))
+// Pass B's row FFT of M_kappa' yields conj(Z[-k]) at the same frequencies as
+// the P row, so the two real columns are separated in pass B's registers.
+struct PMOut {
+  double2* TP;  // P plane of this pair at this n2 (+ rho)
+  double2* TM;  // M plane
+  cplx cn2;     // W_L^(n2 K) = W_N2^(n2)
+};
+
+__device__ __forceinline__ void emit_pm(const PassAArgs& a, const PMOut& o, int N1, int d, int j, int k1, cplx Y,
+                                        cplx w) {
+  if (a.dbg & 1) return;
+  const cplx Yw = cmul(Y, w);
+  if (k1 < a.res_cnt[j]) sts_c(o.TP + a.res_base[j] + k1, Yw);
+  if (j == 0) {
+    if (k1 == 0) {
+      sts_c(o.TM + a.res_base[0], cconj(Y));
+    } else if (2 * k1 >= N1) {
+      sts_c(o.TM + a.res_base[0] + (N1 - k1), cmul(cconj(Yw), o.cn2));
+    }
+  } else if (2 * k1 >= N1) {
+    sts_c(o.TM + a.res_base[d - j] + (N1 - 1 - k1), cmul(cconj(Yw), o.cn2));
+  }
+}
+
+// Small column transforms (T < 32 threads per column): one CTA = one column
+// pair x G adjacent columns; residues transformed in sequence.
 template <int N1>
-__global__ void __launch_bounds__(512, 1) passA_kernel(const PassAArgs a) {
+__global__ void __launch_bounds__(256) passA_kernel(const PassAArgs a) {
   constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1);
   extern __shared__ double2 smem[];
-  __shared__ double red[2][512];
-  __shared__ double2 Pst[16];
-  const int GT = blockDim.x >> 1;  // threads per group
-  const int G = GT / T;            // columns per CTA
-  const int tid = threadIdx.x, grp = tid >= GT ? 1 : 0, lt = tid - grp * GT;
-  const int g = lt / T, t = lt - g * T;
+  __shared__ double red[2][256];
+  const int G = blockDim.x / T;
+  const int tid = threadIdx.x, g = tid / T, t = tid - g * T;
   const int n2 = blockIdx.x * G + g;
   const int pair = blockIdx.y;
   const int d = a.d;
+  const size_t Np = (size_t)N1 * a.N2;
   double2* zbuf = smem;
-  double2* buf0 = smem + G * N1;
-  double2* buf1 = buf0 + G * SE;
-  double2* mybuf = (grp ? buf1 : buf0) + g * SE;
-  double2* otbuf = (grp ? buf0 : buf1) + g * SE;
+  double2* exch = smem + G * N1 + g * SE;
   const double2* zc = zbuf + g * N1;
-
-  // stage z and reduce the column sums (loss operator), coalesced over G*N1
   {
-    const size_t Np = (size_t)N1 * a.N2;
     const size_t e0 = (size_t)blockIdx.x * G * N1;
     const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
     const double* xb = xa + Np;
     double sa = 0.0, sb = 0.0;
-    const double2* xa2 = reinterpret_cast<const double2*>(xa);
-    const double2* xb2 = reinterpret_cast<const double2*>(xb);
-    const double2* nv2 = reinterpret_cast<const double2*>(a.nv + e0);
-    const double2* kv2 = a.kv ? reinterpret_cast<const double2*>(a.kv + e0) : nullptr;
-#pragma unroll 4
-    for (int i = tid; i < G * N1 / 2; i += blockDim.x) {
-      double2 w = __ldg(nv2 + i);
-      if (kv2) {
-        const double2 k = __ldg(kv2 + i);
-        w.x = __dadd_rn(w.x, __dmul_rn(a.alpha, k.x));
-        w.y = __dadd_rn(w.y, __dmul_rn(a.alpha, k.y));
-      }
-      const double2 ua = __ldg(xa2 + i), ub = __ldg(xb2 + i);
-      const double va0 = ua.x * w.x, va1 = ua.y * w.y, vb0 = ub.x * w.x, vb1 = ub.y * w.y;
-      zbuf[2 * i] = make_double2(va0, vb0);
-      zbuf[2 * i + 1] = make_double2(va1, vb1);
-      sa += va0 + va1;
-      sb += vb0 + vb1;
+    for (int i = tid; i < G * N1; i += blockDim.x) {
+      const double w = state_at(a.nv, a.kv, a.alpha, e0 + i);
+      const double va = __ldg(xa + i) * w, vb = __ldg(xb + i) * w;
+      zbuf[i] = make_double2(va, vb);
+      sa += va;
+      sb += vb;
     }
     red[0][tid] = sa;
     red[1][tid] = sb;
     __syncthreads();
-    for (int w = 256; w > 0; w >>= 1) {
+    for (int w = 128; w > 0; w >>= 1) {
       if (tid < w && tid + w < (int)blockDim.x) {
         red[0][tid] += red[0][tid + w];
         red[1][tid] += red[1][tid + w];
@@ -287,98 +295,23 @@ __global__ void __launch_bounds__(512, 1) passA_kernel(const PassAArgs a) {
     }
   }
   if (!a.want_T) return;
-  // G == 1: row twiddle W_L^(n2 kappa) = base(thread, residue) * P[r], P[r] = W_L^(n2 d T r)
-  if (G == 1 && tid < 16) {
-    const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * tid);
-    Pst[tid] = make_double2(w.x, w.y);
-  }
-  __syncthreads();
-
-  const size_t colT = (size_t)a.K_rows * a.N2;
-  double2* Ta = a.T + (size_t)(2 * pair) * colT + (size_t)n2 * a.K_rows;  // exchange layout T[c][n2][rho]
-  double2* Tb = Ta + colT;
-  // w = W_L^(n2 kappa); separate the two real columns, twiddle, store
-  auto emit = [&](int j, int k1, cplx Z, cplx Zm, cplx w) {
-    const cplx cz = cconj(Zm);
-    const cplx A = cscale(cadd(Z, cz), 0.5);
-    const cplx B = cscale(mul_mi(csub(Z, cz)), 0.5);
-    const int rho = a.res_base[j] + k1;
-    const size_t off = rho;
-    sts_c(Ta + off, cmul(A, w));
-    sts_c(Tb + off, cmul(B, w));
-  };
-  auto rowtw = [&](int kappa_base, int r, bool down) -> cplx {
-    // W_L^(n2 * (kappa_base +/- d*T*r))
-    if (G == 1) {
-      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kappa_base);
-      const cplx p = lds_c(Pst + r);
-      return down ? cmulc(b, p) : cmul(b, p);
-    }
-    const int kap = down ? kappa_base - d * T * r : kappa_base + d * T * r;
-    return twL(a.tabLlo, a.tabLhi, (long long)n2 * kap);
-  };
-  const GroupSync gs{1 + grp, GT};
-
-  // residue pairs (j, d-j), 0 < j < d/2: group 0 transforms residue j,
-  // group 1 residue d-j; together they emit all N1 rows of residue j
-  for (int j = 1; 2 * j < d; ++j) {
-    const int jr = grp ? d - j : j;
+  const size_t plane = (size_t)a.K_rows * a.N2;
+  PMOut o;
+  o.TP = a.T + (size_t)pair * 2 * plane + (size_t)n2 * a.K_rows;
+  o.TM = o.TP + plane;
+  o.cn2 = twL(a.tabLlo, a.tabLhi, (long long)n2 * (d * N1));
+  for (int j = 0; j < d; ++j) {
     cplx v[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       const int n1 = t + T * r;
-      v[r] = cmul(lds_c(zc + n1), ld_c(a.tabK + jr * n1));
+      v[r] = cmul(lds_c(zc + n1), ld_c(a.tabK + j * n1));
     }
-    fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
+    fft_fwd<N1>(v, t, exch, a.tw);
 #pragma unroll
-    for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
-    __syncthreads();
-    if (grp == 0) {
-      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * (j + d * t));
-#pragma unroll
-      for (int r = 0; r < E / 2; ++r) {
-        const int k1 = t + T * r;
-        const cplx w = G == 1 ? cmul(b, lds_c(Pst + r)) : rowtw(j + d * t, r, false);
-        emit(j, k1, v[r], lds_c(otbuf + pad16(N1 - 1 - k1)), w);
-      }
-    } else {
-      const int kb = j + d * (N1 - 1 - t);
-      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kb);
-#pragma unroll
-      for (int r = 0; r < E / 2; ++r) {
-        const int k1 = N1 - 1 - (t + T * r);
-        const cplx w = G == 1 ? cmulc(b, lds_c(Pst + r)) : rowtw(kb, r, true);
-        emit(j, k1, lds_c(otbuf + pad16(k1)), v[r], w);
-      }
-    }
-    __syncthreads();
-  }
-  // self-mirrored residues: 0 on group 0, d/2 (even d) on group 1
-  {
-    const int jr = grp == 0 ? 0 : ((d & 1) ? -1 : d / 2);
-    if (jr >= 0) {
-      cplx v[E];
-#pragma unroll
-      for (int r = 0; r < E; ++r) {
-        const int n1 = t + T * r;
-        v[r] = jr == 0 ? lds_c(zc + n1) : cmul(lds_c(zc + n1), ld_c(a.tabK + jr * n1));
-      }
-      fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
-#pragma unroll
-      for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
-      if (GT >= 32) gs(); else __syncwarp();
-      const int kb = jr + d * t;
-      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kb);
-#pragma unroll
-      for (int r = 0; r < E; ++r) {
-        const int k1 = t + T * r;
-        const bool keep = jr == 0 ? (2 * k1 <= N1) : (2 * k1 < N1);
-        if (keep) {
-          const cplx w = G == 1 ? cmul(b, lds_c(Pst + (r & 15))) : rowtw(kb, r, false);
-          const int mk = jr == 0 ? ((N1 - k1) & (N1 - 1)) : (N1 - 1 - k1);
-          emit(jr, k1, v[r], lds_c(mybuf + pad16(mk)), w);
-        }
-      }
+    for (int r = 0; r < E; ++r) {
+      const int k1 = t + T * r;
+      emit_pm(a, o, N1, d, j, k1, v[r], twL(a.tabLlo, a.tabLhi, (long long)n2 * (j + d * k1)));
     }
   }
 }
@@ -388,69 +321,65 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Persistent pass A for column transforms of >= 32 threads (N1 >= 512): one
-// work item = (column pair, n2).  Two thread groups transform residues j and
-// d-j concurrently and separate the two real columns through the Hermitian
-// mirror (one CTA barrier per round besides the FFT's group barriers); the
-// next item's inputs are prefetched into L2 at the start of each item.
+// Pass A for column transforms of >= 32 threads (N1 >= 512): one CTA (one
+// thread group, T threads) = one work item (column pair, n2), 70 KB of shared
+// memory, two CTAs per SM so one CTA's memory phases overlap the other's
+// FFTs.  The weighted input z = (a + i b) n is re-read from L2 for every
+// residue (first touch from DRAM); outputs leave as P/M exchange rows.
 template <int N1>
-__global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassAArgs a, int nitems) {
-  constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1), H = N1 / 2;
-  constexpr int NW = 2 * T / 32;
+__global__ void __launch_bounds__(fft_t(N1), 2) passA_big_kernel(const PassAArgs a) {
+  constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1);
+  constexpr int NW = T / 32;
   static_assert(T >= 32, "warp-multiple groups");
   extern __shared__ double2 smem[];
   __shared__ double red[2][NW];
   __shared__ double2 Pst[16];
-  __shared__ double2 Kst[MAXRES * 2][16];  // W_K^(j T r): twist steps per residue
-  const int tid = threadIdx.x, grp = tid >= T ? 1 : 0, t = tid - grp * T;
-  const int lane = tid & 31, wid = tid >> 5;
+  __shared__ double2 Kst[MAXRES][16];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int d = a.d;
   const int N2 = a.N2;
-  double2* zbuf = smem;
-  double2* buf0 = smem + N1;
-  double2* buf1 = buf0 + SE;
-  double2* mybuf = grp ? buf1 : buf0;
-  double2* otbuf = grp ? buf0 : buf1;
+  const int K = d * N1;
+  const int item = blockIdx.x;
+  const int pair = item / N2, n2 = item - pair * N2;
   const size_t Np = (size_t)N1 * N2;
-  const size_t colT = (size_t)a.K_rows * N2;
-  const GroupSync gs{1 + grp, T};
-  for (int i = tid; i < d * 16; i += blockDim.x) {
+  const size_t e0 = (size_t)n2 * N1;
+  const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
+  const double* xb = xa + Np;
+  const double* nv = a.nv + e0;
+  const double* kv = a.kv ? a.kv + e0 : nullptr;
+  double2* exch = smem;
+  for (int i = t; i < d * 16; i += T) {
     const int j = i / 16, r = i % 16;
-    const cplx w = ld_c(a.tabK + (j * T * r) % (d * N1));
+    const cplx w = ld_c(a.tabK + (j * T * r) % K);
     Kst[j][r] = make_double2(w.x, w.y);
   }
-  // twist base W_K^(j t) of this thread for residue j (one table load)
-  auto twist_base = [&](int j) { return ld_c(a.tabK + j * t); };
-
-  // stage z = (a + i b) * n of `it` into zbuf with threads [first, first+nthr)
-  // and reduce its two column sums (warp shuffles, one barrier `bar`)
-  auto stage = [&](int it, int first, int nthr, auto&& bar) {
-    const int pp = it / N2, nn = it - pp * N2;
-    const size_t e = (size_t)nn * N1;
-    const double2* xa2 = reinterpret_cast<const double2*>(a.X + (size_t)(2 * pp) * Np + e);
-    const double2* xb2 = reinterpret_cast<const double2*>(a.X + (size_t)(2 * pp + 1) * Np + e);
-    const double2* nv2 = reinterpret_cast<const double2*>(a.nv + e);
-    const double2* kv2 = a.kv ? reinterpret_cast<const double2*>(a.kv + e) : nullptr;
-    const int me = tid - first;
+  if (t < 16) {
+    const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * t);
+    Pst[t] = make_double2(w.x, w.y);
+  }
+  const size_t plane = (size_t)a.K_rows * N2;
+  PMOut o;
+  o.TP = a.T + (size_t)pair * 2 * plane + (size_t)n2 * a.K_rows;
+  o.TM = o.TP + plane;
+  o.cn2 = twL(a.tabLlo, a.tabLhi, (long long)n2 * K);
+  // z in the FFT's register layout (element t + T r)
+  auto load_z = [&](cplx (&z)[E]) {
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int n1 = t + T * r;
+      double w = __ldg(nv + n1);
+      if (kv) w = __dadd_rn(w, __dmul_rn(a.alpha, __ldg(kv + n1)));
+      z[r] = mk(__ldg(xa + n1) * w, __ldg(xb + n1) * w);
+    }
+  };
+  {
+    cplx z[E];
+    load_z(z);
     double sa = 0.0, sb = 0.0;
-#pragma unroll 4
-    for (int i = me; i < N1 / 2; i += nthr) {
-      double2 w = make_double2(1.0, 1.0), ua = make_double2(i, 1.0), ub = make_double2(1.0, i);
-      if (!(a.dbg & 4)) {
-        w = __ldg(nv2 + i);
-        if (kv2) {
-          const double2 k = __ldg(kv2 + i);
-          w.x = __dadd_rn(w.x, __dmul_rn(a.alpha, k.x));
-          w.y = __dadd_rn(w.y, __dmul_rn(a.alpha, k.y));
-        }
-        ua = __ldg(xa2 + i);
-        ub = __ldg(xb2 + i);
-      }
-      const double va0 = ua.x * w.x, va1 = ua.y * w.y, vb0 = ub.x * w.x, vb1 = ub.y * w.y;
-      zbuf[2 * i] = make_double2(va0, vb0);
-      zbuf[2 * i + 1] = make_double2(va1, vb1);
-      sa += va0 + va1;
-      sb += vb0 + vb1;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      sa += z[r].x;
+      sb += z[r].y;
     }
     sa = warp_sum(sa);
     sb = warp_sum(sb);
@@ -458,119 +387,33 @@ __global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_tma_kernel(const PassA
       red[0][wid] = sa;
       red[1][wid] = sb;
     }
-    bar();
-    if (me == 0) {
+    __syncthreads();
+    if (t == 0) {
       double ta = 0.0, tb = 0.0;
-      for (int w = first / 32; w < (first + nthr) / 32; ++w) {
+      for (int w = 0; w < NW; ++w) {
         ta += red[0][w];
         tb += red[1][w];
       }
-      a.dots[(size_t)(2 * pp) * a.nblk + nn] = ta;
-      a.dots[(size_t)(2 * pp + 1) * a.nblk + nn] = tb;
+      a.dots[(size_t)(2 * pair) * a.nblk + n2] = ta;
+      a.dots[(size_t)(2 * pair + 1) * a.nblk + n2] = tb;
     }
-  };
-  auto cta_bar = [&]() { __syncthreads(); };
-  bool staged = false;  // zbuf already holds this item's z (staged during the previous item)
-
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int pair = item / N2, n2 = item - pair * N2;
-    const int next = item + gridDim.x;
-    if (tid == 0) {
-      const int nx = staged ? next : item + gridDim.x;
-      if (nx < nitems) {
-        const int np_ = nx / N2, nn2 = nx - np_ * N2;
-        const double* nxa = a.X + (size_t)(2 * np_) * Np + (size_t)nn2 * N1;
-        prefetch_l2(nxa, N1 * 8);
-        prefetch_l2(nxa + Np, N1 * 8);
-        prefetch_l2(a.nv + (size_t)nn2 * N1, N1 * 8);
-        if (a.kv) prefetch_l2(a.kv + (size_t)nn2 * N1, N1 * 8);
-      }
-    }
-    if (!staged) stage(item, 0, 2 * T, cta_bar);
-    if (tid < 16) {
-      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * tid);
-      Pst[tid] = make_double2(w.x, w.y);
-    }
-    __syncthreads();
-    double2* Ta = a.T + (size_t)(2 * pair) * colT + (size_t)n2 * a.K_rows;
-    double2* Tb = Ta + colT;
-    auto emit = [&](int rho, cplx Z, cplx Zm, cplx w) {
-      const cplx cz = cconj(Zm);
-      const cplx A = cscale(cadd(Z, cz), 0.5);
-      const cplx B = cscale(mul_mi(csub(Z, cz)), 0.5);
-      if (!(a.dbg & 1)) {
-        sts_c(Ta + rho, cmul(A, w));
-        sts_c(Tb + rho, cmul(B, w));
-      }
-    };
-
-    // residue pairs (j, d-j), 0 < j < d/2
-    for (int j = 1; 2 * j < d; ++j) {
-      const int jr = grp ? d - j : j;
-      cplx v[E];
-      {
-        const cplx tb = twist_base(jr);
+    if (!a.want_T) return;
+    // residue 0 straight from these registers
+    fft_fwd<N1>(z, t, exch, a.tw);
+    const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * (d * t));
 #pragma unroll
-        for (int r = 0; r < E; ++r)
-          v[r] = cmul(lds_c(zbuf + t + T * r), cmul(tb, lds_c(&Kst[jr][r])));
-      }
-      if (!(a.dbg & 2)) fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
+    for (int r = 0; r < E; ++r) emit_pm(a, o, N1, d, 0, t + T * r, z[r], cmul(b, lds_c(Pst + r)));
+  }
+  for (int j = 1; j < d; ++j) {
+    cplx v[E];
+    load_z(v);
+    const cplx tb = ld_c(a.tabK + j * t);
 #pragma unroll
-      for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
-      __syncthreads();
-      // group 0: rows k1 = t + T r (< H); group 1: rows k1 = N1-1-(t + T r) (>= H)
-      const int kb = grp ? j + d * (N1 - 1 - t) : j + d * t;
-      const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * kb);
-      const int rho0 = a.res_base[j];
+    for (int r = 0; r < E; ++r) v[r] = cmul(v[r], cmul(tb, lds_c(&Kst[j][r])));
+    fft_fwd<N1>(v, t, exch, a.tw);
+    const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * (j + d * t));
 #pragma unroll
-      for (int r = 0; r < E / 2; ++r) {
-        const int kk = t + T * r;
-        const cplx o = lds_c(otbuf + pad16(N1 - 1 - kk));
-        if (grp == 0) {
-          emit(rho0 + kk, v[r], o, cmul(b, lds_c(Pst + r)));
-        } else {
-          emit(rho0 + N1 - 1 - kk, o, v[r], cmulc(b, lds_c(Pst + r)));
-        }
-      }
-      __syncthreads();  // buffers are rewritten by the next round's FFTs
-    }
-    // self-mirrored residues: 0 on group 0 (rows k1 <= H), d/2 (even d) on group 1 (rows k1 < H);
-    // for odd d group 1 is free and stages the next item once group 0 has read zbuf
-    const bool overlap = (d & 1) && next < nitems;
-    {
-      const int jr = grp == 0 ? 0 : ((d & 1) ? -1 : d / 2);
-      if (grp == 1 && overlap) {
-        asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");  // group 0 has its z in registers
-        stage(next, T, T, gs);
-      }
-      if (jr >= 0) {
-        cplx v[E];
-        const cplx tb = twist_base(jr);
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-          const cplx z = lds_c(zbuf + t + T * r);
-          v[r] = jr == 0 ? z : cmul(z, cmul(tb, lds_c(&Kst[jr][r])));
-        }
-        if (grp == 0 && overlap) asm volatile("bar.arrive 3, %0;" ::"r"(2 * T) : "memory");
-        if (!(a.dbg & 2)) fft_fwd<N1, GroupSync>(v, t, mybuf, a.tw, gs);
-#pragma unroll
-        for (int r = 0; r < E; ++r) sts_c(mybuf + pad16(t + T * r), v[r]);
-        gs();
-        const int cnt = jr == 0 ? H + 1 : H;
-        const cplx b = twL(a.tabLlo, a.tabLhi, (long long)n2 * (jr + d * t));
-        const int rho0 = a.res_base[jr];
-#pragma unroll
-        for (int r = 0; r <= E / 2; ++r) {
-          const int k1 = t + T * r;
-          if (k1 < cnt) {
-            const int mk = jr == 0 ? ((N1 - k1) & (N1 - 1)) : (N1 - 1 - k1);
-            emit(rho0 + k1, v[r], lds_c(mybuf + pad16(mk)), cmul(b, lds_c(Pst + (r & 15))));
-          }
-        }
-      }
-    }
-    __syncthreads();  // zbuf and the buffers are rewritten by the next item
-    staged = overlap;
+    for (int r = 0; r < E; ++r) emit_pm(a, o, N1, d, j, t + T * r, v[r], cmul(b, lds_c(Pst + r)));
   }
 }
 
@@ -592,7 +435,9 @@ struct PassBArgs {
 
 // One CTA = 8 exchange rows x T threads per row (128 threads).  Lanes run
 // over the 8 rows fastest so every warp load reads whole 128-byte segments
-// of T[c][n2][rho]; the row transforms exchange through shared memory.
+// of the P and M planes T[pair][plane][n2][rho]; the row transforms exchange
+// through shared memory.  Per column pair: FFT(P row), FFT(M row), then the
+// two real columns separate in registers: A = (P + M)/2, B = -i (P - M)/2.
 template <int N2, bool TT>
 __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   constexpr int E = fft_e(N2), T = fft_t(N2), SE = fft_smem_elems(N2);
@@ -604,81 +449,103 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   const int rho = blockIdx.x * ROWS + rloc;
   const bool valid = rho < a.K_rows;
   double2* exch = smem + rloc * SE;
-  const size_t colT = (size_t)a.K_rows * N2;
-  const double2* Tb = a.T + rho;  // + c*colT + n2*K_rows
+  double2* Sb = smem + ROWS * SE;  // CP rank sum, [k2][row] (conflict-free across the rows of a warp)
+  const size_t plane = (size_t)a.K_rows * N2;
+  const double2* Tb = a.T + rho;  // + pair*2*plane + {0, plane} + n2*K_rows
 
-  cplx S[E], prod[E];
+  cplx S[E], acc[E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     S[i] = mk(0.0, 0.0);
-    prod[i] = mk(0.0, 0.0);
+    acc[i] = mk(0.0, 0.0);
   }
   const int d = a.d;
   const int C = a.C;
-
+  const int npairs = (C + 1) / 2;
   if constexpr (!TT) {
-    int m = 0;
-    for (int c = 0; c < C; ++c) {
-      cplx v[E];
-      const double2* src = Tb + (size_t)c * colT;
 #pragma unroll
-      for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
-      fft_fwd<N2>(v, t, exch, a.tw);
+    for (int i = 0; i < E; ++i) Sb[(t + T * i) * ROWS + rloc] = make_double2(0.0, 0.0);
+  }
+  // TT: fiber c -> (core lam, rn, rp), tracked incrementally
+  int lam = 0, rn = 0, rp = 0;
+  const size_t slot = (size_t)blockIdx.x * 2 * a.Rmax;
+  auto st = [&](int b, int r, int i) -> double2* {
+    return a.scratch + ((slot + (size_t)b * a.Rmax + r) * E + i) * blockDim.x + tid;
+  };
+
+  auto process = [&](cplx (&X)[E], int c) {
+    if constexpr (!TT) {
+      const int m = c % d;  // rank-major columns: c = r d + m
       if (m == 0) {
 #pragma unroll
-        for (int i = 0; i < E; ++i) prod[i] = v[i];
+        for (int i = 0; i < E; ++i) acc[i] = X[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < E; ++i) prod[i] = cmul(prod[i], v[i]);
+        for (int i = 0; i < E; ++i) acc[i] = cmul(acc[i], X[i]);
       }
       if (m == d - 1) {
 #pragma unroll
-        for (int i = 0; i < E; ++i) S[i] = cadd(S[i], prod[i]);
-        m = 0;
-      } else {
-        ++m;
+        for (int i = 0; i < E; ++i) {
+          double2* sp = Sb + (t + T * i) * ROWS + rloc;
+          sts_c(sp, cadd(lds_c(sp), acc[i]));
+        }
       }
-    }
-  } else {
-    // TT chain; state vectors in a private global scratch (coalesced per thread slot)
-    const size_t slot = (size_t)blockIdx.x * 2 * a.Rmax;
-    auto st = [&](int b, int r, int i) -> double2* {
-      return a.scratch + ((slot + (size_t)b * a.Rmax + r) * E + i) * blockDim.x + tid;
-    };
-    int c = 0, in = 0;
-    for (int lam = 0; lam < d; ++lam) {
-      const int rp_n = a.ranks[lam], rn_n = a.ranks[lam + 1];
-      for (int rn = 0; rn < rn_n; ++rn) {
-        for (int rp = 0; rp < rp_n; ++rp, ++c) {
-          cplx v[E];
-          const double2* src = Tb + (size_t)c * colT;
+    } else {
+      const int rp_n = a.ranks[lam];
+      if (lam == 0) {
 #pragma unroll
-          for (int i = 0; i < E; ++i) v[i] = valid ? ld_c(src + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
-          fft_fwd<N2>(v, t, exch, a.tw);
-          if (lam == 0) {
+        for (int i = 0; i < E; ++i) sts_c(st(0, rn, i), X[i]);
+      } else {
+        if (rp == 0) {
 #pragma unroll
-            for (int i = 0; i < E; ++i) sts_c(st(in, rn, i), v[i]);
+          for (int i = 0; i < E; ++i) acc[i] = mk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(lds_c(st((lam - 1) & 1, rp, i)), X[i]));
+        if (rp == rp_n - 1) {
+          if (lam == d - 1) {
+#pragma unroll
+            for (int i = 0; i < E; ++i) S[i] = acc[i];
           } else {
-            if (rp == 0) {
 #pragma unroll
-              for (int i = 0; i < E; ++i) prod[i] = mk(0.0, 0.0);
-            }
-#pragma unroll
-            for (int i = 0; i < E; ++i) prod[i] = cadd(prod[i], cmul(lds_c(st(in, rp, i)), v[i]));
-            if (rp == rp_n - 1) {
-              if (lam == d - 1) {
-#pragma unroll
-                for (int i = 0; i < E; ++i) S[i] = prod[i];
-              } else {
-#pragma unroll
-                for (int i = 0; i < E; ++i) sts_c(st(in ^ 1, rn, i), prod[i]);
-              }
-            }
+            for (int i = 0; i < E; ++i) sts_c(st(lam & 1, rn, i), acc[i]);
           }
         }
       }
-      if (lam > 0) in ^= 1;
+      // advance (lam, rn, rp) in fiber order: rn-major, rp inner
+      if (++rp == rp_n) {
+        rp = 0;
+        if (++rn == a.ranks[lam + 1]) {
+          rn = 0;
+          ++lam;
+        }
+      }
     }
+  };
+
+  for (int p = 0; p < npairs; ++p) {
+    cplx vp[E], vm[E];
+    const double2* srcP = Tb + (size_t)p * 2 * plane;
+    const double2* srcM = srcP + plane;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      vp[i] = valid ? ld_c(srcP + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
+      vm[i] = valid ? ld_c(srcM + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
+    }
+    fft_fwd<N2>(vp, t, exch, a.tw);
+    fft_fwd<N2>(vm, t, exch, a.tw);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const cplx P = vp[i];
+      vp[i] = cscale(cadd(P, vm[i]), 0.5);
+      vm[i] = cscale(mul_mi(csub(P, vm[i])), 0.5);
+    }
+    process(vp, 2 * p);
+    if (2 * p + 1 < C) process(vm, 2 * p + 1);
+  }
+  if constexpr (!TT) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) S[i] = lds_c(Sb + (t + T * i) * ROWS + rloc);
   }
 
   // (d-1)-position shift (s'[t] = s[t-(d-1)] <=> S'[k] = S[k] W_L^{(d-1)k}), inverse row FFT, inverse twiddle, Hermitian weight
@@ -1129,9 +996,9 @@ int get_plan(ttagg_ctx* ctx, int d, const Geom& g, OrderPlan** out) {
     base += (cnt + RB - 1) & ~(RB - 1);
     ++nres;
   };
+  // rows kappa in [0, K/2] grouped by residue j = kappa mod d (kappa = j + d k1)
   add(N1 / 2 + 1);
-  for (int j = 1; 2 * j < d; ++j) add(N1);
-  if ((d & 1) == 0) add(N1 / 2);
+  for (int j = 1; j < d; ++j) add(N1 / 2);
   P->nres = nres;
   P->K_rows = base;
   std::vector<int> kap(P->K_rows, -1);
@@ -1173,33 +1040,23 @@ int set_smem(K kern, size_t bytes) {
 
 // ---- pass A
 // columns per pass-A CTA: thread groups of <= 128 threads when the transform allows
-constexpr int passA_G(int T, int N2) { return std::max(1, std::min(128 / T, N2)); }
+constexpr int passA_G(int T, int N2) { return std::max(1, std::min(256 / T, N2)); }
 
 template <int N1>
 int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   constexpr int T = fft_t(N1);
   if constexpr (T >= 32) {
-    static int nsm = 0, occ = 0;
-    const size_t smem = ((size_t)N1 + 2 * (size_t)fft_smem_elems(N1)) * sizeof(double2);
-    TRY(set_smem(passA_tma_kernel<N1>, smem));
-    if (!nsm) {
-      int dev = 0;
-      CUDA_TRY(cudaGetDevice(&dev));
-      CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passA_tma_kernel<N1>, 2 * T, smem));
-      occ = std::max(occ, 1);
-    }
-    const int nitems = npairs * N2;
-    const int grid = std::min(nitems, nsm * occ);
-    passA_tma_kernel<N1><<<grid, 2 * T, smem, st>>>(a, nitems);
+    const size_t smem = (size_t)fft_smem_elems(N1) * sizeof(double2);
+    TRY(set_smem(passA_big_kernel<N1>, smem));
+    passA_big_kernel<N1><<<npairs * N2, T, smem, st>>>(a);
     CUDA_TRY(cudaGetLastError());
     return TTAGG_OK;
   }
   const int G = passA_G(T, N2);
-  const size_t smem = ((size_t)G * N1 + (size_t)2 * G * fft_smem_elems(N1)) * sizeof(double2);
+  const size_t smem = ((size_t)G * N1 + (size_t)G * fft_smem_elems(N1)) * sizeof(double2);
   TRY(set_smem(passA_kernel<N1>, smem));
   dim3 grid(N2 / G, npairs);
-  passA_kernel<N1><<<grid, 2 * T * G, smem, st>>>(a);
+  passA_kernel<N1><<<grid, T * G, smem, st>>>(a);
   CUDA_TRY(cudaGetLastError());
   return TTAGG_OK;
 }
@@ -1228,7 +1085,7 @@ template <int N2, bool TT>
 int launchB(const PassBArgs& a, cudaStream_t st) {
   constexpr int T = fft_t(N2);
   constexpr int ROWS = 128 / T;
-  const size_t smem = (size_t)ROWS * fft_smem_elems(N2) * sizeof(double2);
+  const size_t smem = ((size_t)ROWS * fft_smem_elems(N2) + (size_t)ROWS * N2) * sizeof(double2);
   TRY(set_smem(passB_kernel<N2, TT>, smem));
   const int grid = (a.K_rows + ROWS - 1) / ROWS;
   passB_kernel<N2, TT><<<grid, 128, smem, st>>>(a);
