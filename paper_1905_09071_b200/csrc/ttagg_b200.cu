@@ -704,24 +704,24 @@ __device__ __forceinline__ void pq_at(const CombineArgs& A, size_t e, double nvv
     if (o.coef) {
       // loads batched 8 at a time, summed in rank order (deterministic)
       double tail = 0.0;
-      for (int r0 = 0; r0 < o.ntail; r0 += 8) {
-        double xv[8], cv[8];
+      constexpr int BT = 24;
+      for (int r0 = 0; r0 < o.ntail; r0 += BT) {
+        double xv[BT];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < BT; ++u) {
           const int r = r0 + u;
           xv[u] = r < o.ntail ? __ldg(o.X + (size_t)__ldg(o.tail + r) * Np + e) : 0.0;
-          cv[u] = r < o.ntail ? __ldg(o.coef + r) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (r0 + u < o.ntail) tail += xv[u] * cv[u];
+        for (int u = 0; u < BT; ++u)
+          if (r0 + u < o.ntail) tail += xv[u] * __ldg(o.coef + r0 + u);
       }
       Q += -(nvv * tail) / o.qdiv;
     }
   }
 }
 
-__global__ void __launch_bounds__(256) combine_natural_kernel(const CombineArgs A) {
+__global__ void __launch_bounds__(1024) combine_natural_kernel(const CombineArgs A) {
   __shared__ double tp[32][33], tq[32][33];
   const int TN1 = min(32, A.N1), TN2 = min(32, A.N2);
   const int n1_0 = blockIdx.y * TN1, n2_0 = blockIdx.x * TN2;
@@ -1628,7 +1628,7 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
     ProfScope ps(ctx, 3, st);
     const int TN1 = std::min(32, g.N1), TN2 = std::min(32, g.N2);
     dim3 grid(g.N2 / TN2, g.N1 / TN1);
-    combine_natural_kernel<<<grid, 256, 0, st>>>(A);
+    combine_natural_kernel<<<grid, 1024, 0, st>>>(A);
     CUDA_TRY(cudaGetLastError());
     ++ctx->launches;
   }
