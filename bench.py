@@ -303,7 +303,7 @@ def main():
         if not sharded:
             ks = g.KernelSet({d: g.CPKernel(factors[d]) for d in cfg.orders})
             st = g.ConcentrationState(n0)
-            for _ in range(2):
+            for _ in range(max(4, args.warmup)):
                 g.rhs_total(ks, st)
             t0 = time.perf_counter()
             for _ in range(args.steps):
