@@ -1,0 +1,169 @@
+"""Host-side kernel construction for the BASELINE configs (not on the hot path).
+
+* ``tt_cross`` — TT-cross (alternating maxvol skeletons) of a function on the
+  grid [1..N]^d, for config 4's kernel (i+j+l)^(1/2)(ijl)^(-1/6), which the
+  reference cannot compress (TT-cross is a declared non-goal, SPEC.md:150;
+  SURVEY.md §0.5, §8(f)).  The cores are built once and fed identically to
+  every implementation, so RHS parity never depends on the approximation.
+* ``c4_kernels`` — the C4 kernel set: exact rank-3 TT for (i^(1/3)+j^(1/3))^2
+  (d = 2) and the cross-approximated d = 3 kernel (ranks <= 16, tol 1e-6).
+* ``tt_rank_shard`` — slice a TT kernel over its first internal rank index:
+  the gain and loss are linear in that index (rhs.py:277-290, 305-338), so
+  the slices of all GPUs sum to the full RHS (TT rank sharding).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["maxvol", "tt_cross", "c4_kernels", "tt_rank_shard"]
+
+
+def _orth(a: np.ndarray) -> np.ndarray:
+    """Orthonormal basis of the columns of a tall matrix (CholeskyQR2, O(n r^2))."""
+    q = a
+    for _ in range(2):
+        g = q.T @ q
+        try:
+            r = np.linalg.cholesky(g).T
+        except np.linalg.LinAlgError:
+            return np.linalg.qr(a)[0]
+        q = np.linalg.solve(r.T, q.T).T
+    return q
+
+
+def maxvol(a: np.ndarray, tol: float = 1.05, max_iters: int = 64) -> np.ndarray:
+    """Row indices of a (near) maximum-volume r x r submatrix of the n x r matrix a."""
+    n, r = a.shape
+    if n <= r:
+        return np.arange(n)
+    import scipy.linalg as sla
+
+    # initial guess from LU with partial pivoting (O(n r^2))
+    perm, _, _ = sla.lu(a, p_indices=True)
+    idx = np.array(perm[:r])
+    b = np.linalg.solve(a[idx].T, a.T).T  # n x r, b[idx] = I
+    for _ in range(max_iters):
+        flat = np.argmax(np.abs(b))
+        i, j = divmod(int(flat), r)
+        if abs(b[i, j]) <= tol:
+            break
+        bj = b[:, j].copy()
+        bi = b[i, :].copy()
+        bi[j] -= 1.0
+        b -= np.outer(bj, bi / b[i, j])
+        idx[j] = i
+    return idx
+
+
+def tt_cross(f, n_classes: int, d: int, rank: int, sweeps: int = 2, seed: int = 0):
+    """TT-cross with fixed ranks (1, r, ..., r, 1) of f(idx) on [1..N]^d.
+
+    ``f(points)`` evaluates the function on an (m, d) array of 1-based
+    indices.  Returns d cores of shape (r_{k-1}, N, r_k).
+    """
+    rng = np.random.default_rng(seed)
+    N = n_classes
+    r = [1] + [min(rank, N ** min(k, d - k)) for k in range(1, d)] + [1]
+    grid = np.arange(1, N + 1)
+    # left index sets I[k]: (r[k], k) multi-indices; right sets J[k]: (r[k], d-k)
+    J = [None] * (d + 1)
+    J[d] = np.zeros((1, 0), dtype=np.int64)
+    for k in range(d - 1, 0, -1):
+        J[k] = rng.integers(1, N + 1, size=(r[k], d - k))
+    I = [None] * (d + 1)
+    I[0] = np.zeros((1, 0), dtype=np.int64)
+
+    def fiber(k, Ik, Jk1):
+        # tensor of values f(I_k, i, J_{k+1}) with shape (r_k, N, r_{k+1})
+        if hasattr(f, "fiber"):
+            return f.fiber(Ik, grid, Jk1)
+        a, b = Ik.shape[0], Jk1.shape[0]
+        pts = np.empty((a, N, b, d), dtype=np.int64)
+        pts[:, :, :, :k] = Ik[:, None, None, :]
+        pts[:, :, :, k] = grid[None, :, None]
+        pts[:, :, :, k + 1 :] = Jk1[None, None, :, :]
+        return f(pts.reshape(-1, d)).reshape(a, N, b)
+
+    cores = [None] * d
+    for _ in range(sweeps):
+        # left-to-right: choose I[k+1]
+        for k in range(d - 1):
+            c = fiber(k, I[k], J[k + 1]).reshape(r[k] * N, r[k + 1])
+            sel = maxvol(_orth(c))
+            left = np.concatenate([np.repeat(I[k], N, axis=0), np.tile(grid, r[k])[:, None]], axis=1)
+            I[k + 1] = left[sel]
+        # right-to-left: choose J[k]
+        for k in range(d - 1, 0, -1):
+            c = fiber(k, I[k], J[k + 1]).reshape(r[k], N * r[k + 1])
+            sel = maxvol(_orth(np.ascontiguousarray(c.T)))
+            right = np.concatenate(
+                [np.repeat(grid, r[k + 1])[:, None], np.tile(J[k + 1], (N, 1))], axis=1
+            )
+            J[k] = right[sel]
+    # cores: C_k = f(I_k, :, J_{k+1}) times the inverse of f(I_{k+1}, J_{k+1}) on the right
+    for k in range(d):
+        c = fiber(k, I[k], J[k + 1])
+        if k < d - 1:
+            cmat = c.reshape(r[k] * N, r[k + 1])
+            pts = np.concatenate([I[k + 1], J[k + 1]], axis=1)  # (r_{k+1}, d)
+            # skeleton matrix f(I_{k+1}, J_{k+1}) as (r_{k+1} x r_{k+1}) with rows = I, cols = J
+            a = I[k + 1].shape[0]
+            full = np.empty((a, J[k + 1].shape[0], d), dtype=np.int64)
+            full[:, :, : k + 1] = I[k + 1][:, None, :]
+            full[:, :, k + 1 :] = J[k + 1][None, :, :]
+            m = f(full.reshape(-1, d)).reshape(a, -1)
+            cmat = np.linalg.solve(m.T, cmat.T).T
+            cores[k] = np.ascontiguousarray(cmat.reshape(r[k], N, r[k + 1]))
+        else:
+            cores[k] = np.ascontiguousarray(c)
+    return cores
+
+
+class _C4d3:
+    """(i+j+l)^(1/2) (ijl)^(-1/6): pointwise and broadcast fiber evaluation."""
+
+    def __call__(self, points: np.ndarray) -> np.ndarray:
+        p = points.astype(np.float64)
+        return np.sqrt(p.sum(axis=1)) * np.exp(-np.log(p).sum(axis=1) / 6.0)
+
+    def fiber(self, Ik, grid, Jk1):
+        left = Ik.astype(np.float64)
+        right = Jk1.astype(np.float64)
+        g = grid.astype(np.float64)
+        sl = left.sum(axis=1)[:, None, None]
+        sr = right.sum(axis=1)[None, None, :]
+        pl = np.exp(-np.log(left).sum(axis=1) / 6.0)[:, None, None] if left.shape[1] else 1.0
+        pr = np.exp(-np.log(right).sum(axis=1) / 6.0)[None, None, :] if right.shape[1] else 1.0
+        out = np.sqrt(sl + g[None, :, None] + sr)
+        out *= g[None, :, None] ** (-1.0 / 6.0)
+        out *= pl
+        out *= pr
+        return out
+
+
+_c4_d3 = _C4d3()
+
+
+def c4_kernels(n_classes: int, rank: int = 16, seed: int = 0):
+    """Config 4: {2: exact rank-3 TT of (i^(1/3)+j^(1/3))^2, 3: TT-cross of
+    (i+j+l)^(1/2)(ijl)^(-1/6) with ranks <= rank}; returns (cores2, cores3)."""
+    i = np.arange(1, n_classes + 1, dtype=np.float64)
+    c1 = np.zeros((1, n_classes, 3))
+    c1[0, :, 0], c1[0, :, 1], c1[0, :, 2] = i ** (2 / 3), 2 * i ** (1 / 3), 1.0
+    c2 = np.zeros((3, n_classes, 1))
+    c2[0, :, 0], c2[1, :, 0], c2[2, :, 0] = 1.0, i ** (1 / 3), i ** (2 / 3)
+    cores3 = tt_cross(_c4_d3, n_classes, 3, rank, seed=seed)
+    return (c1, c2), tuple(cores3)
+
+
+def tt_rank_shard(cores, world: int, rank: int):
+    """Cores restricted to this GPU's share of the first internal rank index."""
+    r1 = cores[0].shape[2]
+    sel = np.array_split(np.arange(r1), world)[rank]
+    if sel.size == 0:
+        return None
+    out = list(cores)
+    out[0] = np.ascontiguousarray(cores[0][:, :, sel])
+    out[1] = np.ascontiguousarray(cores[1][sel, :, :])
+    return tuple(out)

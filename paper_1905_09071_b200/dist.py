@@ -21,7 +21,7 @@ import numpy as np
 
 from .parallel import lpt_rank_shards
 
-__all__ = ["shard_for_rank", "CudaEngine", "DistRK2Result", "DistRHS"]
+__all__ = ["shard_for_rank", "tt_shard_for_rank", "CudaEngine", "DistRK2Result", "DistRHS"]
 
 
 def shard_for_rank(rank_counts: dict, world: int, rank: int) -> dict:
@@ -29,10 +29,30 @@ def shard_for_rank(rank_counts: dict, world: int, rank: int) -> dict:
     return lpt_rank_shards(rank_counts, world)[rank]
 
 
-class CudaEngine:
-    """Partial RHS + stage updates on this process's GPU (perm layout)."""
+def tt_shard_for_rank(tt_by_order: dict, world: int, rank: int) -> dict:
+    """{d: cores sliced to this rank's share of the first internal TT rank}.
 
-    def __init__(self, factors_by_order: dict, shard: dict, n_classes: int, device: int):
+    Gain and loss are linear in that index (rhs.py:277-290, 305-338), so the
+    partial RHS of all ranks sums to the full one; orders whose first rank is
+    smaller than the world leave some ranks without a slice."""
+    from .construct import tt_rank_shard
+
+    out = {}
+    for d, cores in tt_by_order.items():
+        sl = tt_rank_shard(cores, world, rank)
+        if sl is not None:
+            out[d] = sl
+    return out
+
+
+class CudaEngine:
+    """Partial RHS + stage updates on this process's GPU (perm layout).
+
+    ``factors_by_order`` / ``shard``: CP factors and this rank's CP rank terms;
+    ``tt_cores``: TT kernels already sliced by :func:`tt_shard_for_rank`."""
+
+    def __init__(self, factors_by_order: dict, shard: dict, n_classes: int, device: int,
+                 tt_cores: dict | None = None):
         import torch
 
         from ._lib import geometry, get_context
@@ -47,6 +67,8 @@ class CudaEngine:
             sub = shard.get(d, [])
             if sub:
                 self.dks.append(self.ctx.upload_cp(factors_by_order[d], rank_subset=sub))
+        for d in sorted(tt_cores or {}):
+            self.dks.append(self.ctx.upload_tt(tt_cores[d]))
         self.diag = torch.zeros(8, dtype=torch.float64, device=self.device)
 
     def vector(self):

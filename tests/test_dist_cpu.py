@@ -13,7 +13,8 @@ import torch.multiprocessing as mp
 
 from conftest import rel_inf
 from oracle import rhs_oracle as orc
-from paper_1905_09071_b200.dist import DistRHS, ideal_speedup, rank_counts_of, shard_for_rank
+from paper_1905_09071_b200.dist import (DistRHS, ideal_speedup, rank_counts_of, shard_for_rank,
+                                         tt_shard_for_rank)
 from paper_1905_09071_b200.parallel import lpt_rank_shards
 from paper_1905_09071_b200.workloads import permutation_power_cp
 
@@ -21,10 +22,11 @@ from paper_1905_09071_b200.workloads import permutation_power_cp
 class OracleEngine:
     """CPU test double of dist.CudaEngine (natural layout torch tensors)."""
 
-    def __init__(self, factors_by_order, shard, n_classes):
+    def __init__(self, factors_by_order, shard, n_classes, tt_cores=None):
         self.f = factors_by_order
         self.shard = shard
         self.n_classes = n_classes
+        self.tt = tt_cores or {}
 
     def vector(self):
         return torch.zeros(self.n_classes, dtype=torch.float64)
@@ -43,6 +45,9 @@ class OracleEngine:
             if sub:
                 acc += orc.cp_gain(self.f[d], x, ranks=sub)
                 acc += orc.cp_loss(self.f[d], x, ranks=sub)
+        for d in sorted(self.tt):
+            acc += orc.tt_gain(self.tt[d], x)
+            acc += orc.tt_loss(self.tt[d], x)
         out.copy_(torch.from_numpy(acc))
 
     def stage(self, base, s, a, out):
@@ -128,3 +133,61 @@ def test_lpt_balance_c5():
             owned = sorted(r for s in shards for r in s.get(d, []))
             assert owned == list(range(R))
         assert shards == lpt_rank_shards(counts, world)  # deterministic
+
+
+def _tt_kernels(N):
+    rng = np.random.default_rng(11)
+    i = np.arange(1, N + 1, dtype=np.float64)
+    c1 = np.zeros((1, N, 3))
+    c1[0, :, 0], c1[0, :, 1], c1[0, :, 2] = i ** (2 / 3), 2 * i ** (1 / 3), 1.0
+    c2 = np.zeros((3, N, 1))
+    c2[0, :, 0], c2[1, :, 0], c2[2, :, 0] = 1.0, i ** (1 / 3), i ** (2 / 3)
+    t3 = (rng.random((1, N, 4)) + 0.5, rng.random((4, N, 3)) + 0.5, rng.random((3, N, 1)) + 0.5)
+    return {2: (c1, c2), 3: t3}
+
+
+def _tt_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N = 200
+        tt = _tt_kernels(N)
+        f = {4: permutation_power_cp((0.1, -0.1, 0.05, 0.0), N)}
+        shard = shard_for_rank(rank_counts_of(f), world, rank)
+        mine = tt_shard_for_rank(tt, world, rank)
+        n0 = np.exp(-np.arange(1, N + 1) / 30.0)
+        n0 = n0 / n0.sum()
+        drhs = DistRHS(OracleEngine(f, shard, N, tt_cores=mine))
+        s = drhs.rhs(torch.from_numpy(n0.copy()))
+        res = drhs.rk2(n0, 0.0, 0.002, 3)
+        q.put((rank, s.numpy(), res.n))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_tt_rank_sharding_matches_unsharded_oracle():
+    """TT kernels sliced over their first internal rank (construct.tt_rank_shard)
+    plus CP rank shards: the all-reduced partials equal the full RHS."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tt_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N = 200
+    tt = _tt_kernels(N)
+    ks = {d: {"kind": "tt", "arrays": v} for d, v in tt.items()}
+    ks[4] = {"kind": "cp", "arrays": permutation_power_cp((0.1, -0.1, 0.05, 0.0), N)}
+    n0 = np.exp(-np.arange(1, N + 1) / 30.0)
+    n0 = n0 / n0.sum()
+    s_ref = orc.rhs_total(ks, n0)[2]
+    n_ref, _, _ = orc.integrate(ks, n0, dt=0.002, steps=3)
+    for _, s, n in out:
+        assert rel_inf(s, s_ref) <= 1e-12
+        assert rel_inf(n, n_ref) <= 1e-12
