@@ -27,7 +27,8 @@ __all__ = [
     "TTAGG_WANT_Q",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libttagg_b200.so")
+# TTAGG_LIB: development override (A/B builds of the same sources with -D switches)
+LIB_PATH = os.environ.get("TTAGG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libttagg_b200.so")
 
 TTAGG_OK = 0
 TTAGG_ERR_ARG = 1

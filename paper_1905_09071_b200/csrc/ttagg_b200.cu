@@ -137,15 +137,21 @@ struct ttagg_ctx {
   std::mutex mu;
   double2* tw4096 = nullptr;
   std::map<std::pair<int, int64_t>, OrderPlan*> plans;
-  // workspaces
-  double2* T = nullptr;
-  size_t T_bytes = 0;
-  double2* U = nullptr;
-  size_t U_bytes = 0;
+  // workspaces: one lane per concurrently running order chain (exchange T,
+  // inverse rows U, TT chain scratch) on its own stream
+  struct Lane {
+    double2* T = nullptr;
+    size_t T_bytes = 0;
+    double2* U = nullptr;
+    size_t U_bytes = 0;
+    double2* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    cudaStream_t s = nullptr;
+    cudaEvent_t done = nullptr;
+  } lane[2];
+  cudaEvent_t ev_fork = nullptr;
   double* pbuf = nullptr;
   size_t pbuf_bytes = 0;
-  double2* scratch = nullptr;
-  size_t scratch_bytes = 0;
   double* vec = nullptr;  // general vectors (natural/perm state, outputs)
   size_t vec_bytes = 0;
   double* diagp = nullptr;  // per-block diag partials
@@ -433,26 +439,47 @@ struct PassBArgs {
   int ranks[MAXD + 1];
 };
 
+// ---- per-thread asynchronous 16-byte copies (global -> shared), zero-fill when !ok
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // One CTA = 8 exchange rows x T threads per row (128 threads).  Lanes run
 // over the 8 rows fastest so every warp load reads whole 128-byte segments
 // of the P and M planes T[pair][plane][n2][rho]; the row transforms exchange
 // through shared memory.  Per column pair: FFT(P row), FFT(M row), then the
 // two real columns separate in registers: A = (P + M)/2, B = -i (P - M)/2.
+// The next pair's planes stream in with cp.async while this pair computes:
+// every thread copies exactly the elements it later reads, into two staging
+// regions that double as the row FFTs' exchange buffers (P stage for FFT(P),
+// M stage for FFT(M)); a plane is re-armed as soon as its FFT has passed the
+// transform's last barrier.
 template <int N2, bool TT>
 __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   constexpr int E = fft_e(N2), T = fft_t(N2), SE = fft_smem_elems(N2);
   constexpr int ROWS = 128 / T;
+  constexpr int STG = (ROWS * SE > E * 128) ? ROWS * SE : E * 128;
   extern __shared__ double2 smem[];
   const int tid = threadIdx.x;
   const int rl8 = tid & 7, t = (tid >> 3) % T, sub = (tid >> 3) / T;
   const int rloc = sub * 8 + rl8;
   const int rho = blockIdx.x * ROWS + rloc;
   const bool valid = rho < a.K_rows;
-  double2* exch = smem + rloc * SE;
-  double2* Sb = smem + ROWS * SE;  // CP rank sum, [k2][row] (conflict-free across the rows of a warp)
+  double2* stP = smem;
+  double2* stM = smem + STG;
+  double2* Sb = smem + 2 * STG;  // CP rank sum, [k2][row] (conflict-free across the rows of a warp)
   const size_t plane = (size_t)a.K_rows * N2;
-  const double2* Tb = a.T + rho;  // + pair*2*plane + {0, plane} + n2*K_rows
-
+  const double2* Tb = a.T + (valid ? rho : 0);  // + pair*2*plane + {0, plane} + n2*K_rows
+  auto fetch = [&](double2* stage, int p, int pl) {
+    const double2* src = Tb + ((size_t)p * 2 + pl) * plane;
+#pragma unroll
+    for (int i = 0; i < E; ++i) cp_async16(stage + i * 128 + tid, src + (size_t)(t + T * i) * a.K_rows, valid);
+    cp_async_commit();
+  };
   cplx S[E], acc[E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
@@ -523,17 +550,23 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     }
   };
 
+  fetch(stP, 0, 0);
+  fetch(stM, 0, 1);
   for (int p = 0; p < npairs; ++p) {
+    const bool more = p + 1 < npairs;
     cplx vp[E], vm[E];
-    const double2* srcP = Tb + (size_t)p * 2 * plane;
-    const double2* srcM = srcP + plane;
+    cp_async_wait<1>();  // P(p) landed (M(p) may still be in flight)
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      vp[i] = valid ? ld_c(srcP + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
-      vm[i] = valid ? ld_c(srcM + (size_t)(t + T * i) * a.K_rows) : mk(0.0, 0.0);
-    }
-    fft_fwd<N2>(vp, t, exch, a.tw);
-    fft_fwd<N2>(vm, t, exch, a.tw);
+    for (int i = 0; i < E; ++i) vp[i] = lds_c(stP + i * 128 + tid);
+    __syncthreads();  // every thread holds its P slots before the stage turns into exchange space
+    fft_fwd<N2>(vp, t, stP + rloc * SE, a.tw);  // ends past its last barrier: stage free again
+    if (more) fetch(stP, p + 1, 0); else cp_async_commit();
+    cp_async_wait<1>();  // M(p) landed
+#pragma unroll
+    for (int i = 0; i < E; ++i) vm[i] = lds_c(stM + i * 128 + tid);
+    __syncthreads();
+    fft_fwd<N2>(vm, t, stM + rloc * SE, a.tw);
+    if (more) fetch(stM, p + 1, 1); else cp_async_commit();
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const cplx P = vp[i];
@@ -543,6 +576,8 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     process(vp, 2 * p);
     if (2 * p + 1 < C) process(vm, 2 * p + 1);
   }
+  cp_async_wait<0>();
+  __syncthreads();
   if constexpr (!TT) {
 #pragma unroll
     for (int i = 0; i < E; ++i) S[i] = lds_c(Sb + (t + T * i) * ROWS + rloc);
@@ -556,7 +591,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     const long long m = ((long long)(d - 1) * k) % a.L;
     S[i] = cmul(S[i], twL(a.tabLlo, a.tabLhi, m));  // shift by d-1: * W_L^{+(d-1)k}
   }
-  fft_inv<N2>(S, t, exch, a.tw);
+  fft_inv<N2>(S, t, stP + rloc * SE, a.tw);
   const double wgt = (kap == 0 || 2 * kap == a.K) ? 1.0 : 2.0;
   if (valid) {
 #pragma unroll
@@ -1085,7 +1120,8 @@ template <int N2, bool TT>
 int launchB(const PassBArgs& a, cudaStream_t st) {
   constexpr int T = fft_t(N2);
   constexpr int ROWS = 128 / T;
-  const size_t smem = ((size_t)ROWS * fft_smem_elems(N2) + (size_t)ROWS * N2) * sizeof(double2);
+  constexpr size_t STG = std::max((size_t)ROWS * fft_smem_elems(N2), (size_t)fft_e(N2) * 128);
+  const size_t smem = (2 * STG + (size_t)ROWS * N2) * sizeof(double2);
   TRY(set_smem(passB_kernel<N2, TT>, smem));
   const int grid = (a.K_rows + ROWS - 1) / ROWS;
   passB_kernel<N2, TT><<<grid, 128, smem, st>>>(a);
@@ -1173,22 +1209,22 @@ struct ProfScope {
 
 // Evaluate the gain of one kernel into pbuf slot and/or its loss coefficients.
 int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const double* kv, double alpha, bool wantP,
-              bool wantQ, double* p_out, cudaStream_t st) {
+              bool wantQ, double* p_out, ttagg_ctx::Lane& ln, cudaStream_t st) {
   const OrderPlan* P = k->plan;
   const Geom& g = k->g;
   const int npairs = k->C_pad / 2;
   if (npairs > 65535) return fail(TTAGG_ERR_UNSUPPORTED, "too many columns for one kernel");
   if (wantP) {
     const size_t need = (size_t)k->C_pad * P->K_rows * g.N2 * sizeof(double2);
-    TRY(ensure((void**)&ctx->T, &ctx->T_bytes, need, true));
-    TRY(ensure((void**)&ctx->U, &ctx->U_bytes, (size_t)P->K_rows * g.N2 * sizeof(double2)));
+    TRY(ensure((void**)&ln.T, &ln.T_bytes, need, true));
+    TRY(ensure((void**)&ln.U, &ln.U_bytes, (size_t)P->K_rows * g.N2 * sizeof(double2)));
   }
   PassAArgs a{};
   a.X = k->X;
   a.nv = nv;
   a.kv = kv;
   a.alpha = alpha;
-  a.T = ctx->T;
+  a.T = ln.T;
   a.dots = k->dots;
   a.tw = ctx->tw4096;
   a.tabK = P->tabK;
@@ -1236,8 +1272,8 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
   }
   if (wantP) {
     PassBArgs b{};
-    b.T = ctx->T;
-    b.U = ctx->U;
+    b.T = ln.T;
+    b.U = ln.U;
     b.tw = ctx->tw4096;
     b.tabLlo = P->tabLlo;
     b.tabLhi = P->tabLhi;
@@ -1254,8 +1290,8 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       const int rows = rowsB(g.N2);
       const int grid = (P->K_rows + rows - 1) / rows;
       const size_t need = (size_t)grid * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
-      TRY(ensure((void**)&ctx->scratch, &ctx->scratch_bytes, need));
-      b.scratch = ctx->scratch;
+      TRY(ensure((void**)&ln.scratch, &ln.scratch_bytes, need));
+      b.scratch = ln.scratch;
     }
     {
       ProfScope ps(ctx, 1, st, k->d);
@@ -1263,7 +1299,7 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       ++ctx->launches;
     }
     PassCArgs c{};
-    c.U = ctx->U;
+    c.U = ln.U;
     c.p = p_out;
     c.tw = ctx->tw4096;
     c.tabK = P->tabK;
@@ -1298,15 +1334,48 @@ int check_set(const ttagg_kernel* const* ks, int nk, Geom* g) {
   return TTAGG_OK;
 }
 
+// Relative device cost of one order's gain (column count x transform length).
+double order_cost(const ttagg_kernel* k) { return (double)std::max(k->C_pad, 1) * k->plan->K_rows; }
+
+int make_lanes(ttagg_ctx* ctx) {
+  if (ctx->lane[0].s) return TTAGG_OK;
+  int lo = 0, hi = 0;
+  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // lane 0 (the most expensive order) at the greatest priority, lane 1 at the least:
+  // lane-1 blocks fill the SMs that lane 0's last wave leaves idle
+  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[0].s, cudaStreamNonBlocking, hi));
+  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[1].s, cudaStreamNonBlocking, lo));
+  for (auto& ln : ctx->lane) CUDA_TRY(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  return TTAGG_OK;
+}
+
 // Run all orders: gains into pbuf, loss coefficients; fill the combine descriptor.
+// With several orders the most expensive order
+// runs on lane 0 and the others, in decreasing cost, on lane 1; both fork
+// from and join back into `st` (also under stream capture).
 int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const double* nv, const double* kv,
                double alpha, bool wantP, bool wantQ, CombineArgs* A, cudaStream_t st) {
   const Geom& g = ks[0]->g;
   if (wantP) TRY(ensure((void**)&ctx->pbuf, &ctx->pbuf_bytes, (size_t)nk * g.Np * sizeof(double)));
-  for (int i = 0; i < nk; ++i) {
+  const bool conc = wantP && nk > 1;
+  int big = 0;
+  for (int i = 1; i < nk; ++i)
+    if (order_cost(ks[i]) > order_cost(ks[big])) big = i;
+  if (conc) {
+    TRY(make_lanes(ctx));
+    CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
+    for (auto& ln : ctx->lane) CUDA_TRY(cudaStreamWaitEvent(ln.s, ctx->ev_fork, 0));
+  }
+  std::vector<int> order(nk);
+  for (int i = 0; i < nk; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int x, int y) { return order_cost(ks[x]) > order_cost(ks[y]); });
+  for (int i : order) {
     const ttagg_kernel* k = ks[i];
     double* pslot = wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr;
-    TRY(run_order(ctx, k, nv, kv, alpha, wantP, wantQ, pslot, st));
+    ttagg_ctx::Lane& ln = ctx->lane[conc && i != big ? 1 : 0];
+    TRY(run_order(ctx, k, nv, kv, alpha, wantP, wantQ, pslot, ln, conc ? ln.s : st));
     CombineOrder& o = A->o[i];
     o.p = pslot;
     o.X = k->X;
@@ -1316,6 +1385,12 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
     double f = 1.0;
     for (int j = 2; j <= k->d - 1; ++j) f *= j;
     o.qdiv = f;
+  }
+  if (conc) {
+    for (auto& ln : ctx->lane) {
+      CUDA_TRY(cudaEventRecord(ln.done, ln.s));
+      CUDA_TRY(cudaStreamWaitEvent(st, ln.done, 0));
+    }
   }
   A->nord = nk;
   A->nv = nv;
@@ -1393,10 +1468,15 @@ int ttagg_ctx_destroy(ttagg_ctx* ctx) {
     delete P;
   }
   cudaFree(ctx->tw4096);
-  cudaFree(ctx->T);
-  cudaFree(ctx->U);
+  for (auto& ln : ctx->lane) {
+    cudaFree(ln.T);
+    cudaFree(ln.U);
+    cudaFree(ln.scratch);
+    if (ln.s) cudaStreamDestroy(ln.s);
+    if (ln.done) cudaEventDestroy(ln.done);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   cudaFree(ctx->pbuf);
-  cudaFree(ctx->scratch);
   cudaFree(ctx->vec);
   cudaFree(ctx->diagp);
   cudaFree(ctx->diag);
