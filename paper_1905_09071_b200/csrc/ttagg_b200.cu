@@ -54,7 +54,12 @@ constexpr int MAXRES = MAXD;  // one residue class per order
 constexpr int MAXORD = 8;
 constexpr int LSPLIT = 11;
 constexpr int LLO = 1 << LSPLIT;
-constexpr int RB = 4;  // residue row blocks are padded to multiples of RB rows
+#ifndef TTAGG_RB
+#define TTAGG_RB 8
+#endif
+// residue row blocks are padded to multiples of RB rows (8 x 16 B: every n2 row of the
+// exchange starts on a 128-byte line, so pass B's 8-row warp loads are whole lines)
+constexpr int RB = TTAGG_RB;
 
 thread_local std::string g_err;
 
