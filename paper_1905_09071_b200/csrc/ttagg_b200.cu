@@ -151,9 +151,15 @@ struct ttagg_ctx {
     size_t U_bytes = 0;
     double2* scratch = nullptr;
     size_t scratch_bytes = 0;
+    double2* Sio = nullptr;  // partial rank sums between pass-B chunks
+    size_t Sio_bytes = 0;
     cudaStream_t s = nullptr;
+    cudaStream_t sB = nullptr;  // pass-B stream of the A/B chunk pipeline
     cudaEvent_t done = nullptr;
+    std::vector<cudaEvent_t> ev;  // per-chunk pass-A completion
+    cudaEvent_t evB = nullptr;
   } lane[2];
+  int num_sms = 0;
   cudaEvent_t ev_fork = nullptr;
   double* pbuf = nullptr;
   size_t pbuf_bytes = 0;
@@ -229,6 +235,7 @@ struct PassAArgs {
   const double2* tabLlo;
   const double2* tabLhi;
   int d, N2, K_rows, nblk, want_T;
+  int pair0;  // first column pair of this launch (pass-A chunk)
   int res_base[MAXRES], res_cnt[MAXRES];
   int dbg;  // debug: 1 skip stores, 2 skip FFTs, 4 skip input loads
 };
@@ -272,7 +279,7 @@ __global__ void __launch_bounds__(256) passA_kernel(const PassAArgs a) {
   const int G = blockDim.x / T;
   const int tid = threadIdx.x, g = tid / T, t = tid - g * T;
   const int n2 = blockIdx.x * G + g;
-  const int pair = blockIdx.y;
+  const int pair = a.pair0 + blockIdx.y;
   const int d = a.d;
   const size_t Np = (size_t)N1 * a.N2;
   double2* zbuf = smem;
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_big_kernel(const PassAArgs
   const int N2 = a.N2;
   const int K = d * N1;
   const int item = blockIdx.x;
-  const int pair = item / N2, n2 = item - pair * N2;
+  const int pair = a.pair0 + item / N2, n2 = item % N2;
   const size_t Np = (size_t)N1 * N2;
   const size_t e0 = (size_t)n2 * N1;
   const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
@@ -439,8 +446,12 @@ struct PassBArgs {
   const double2* tabLhi;
   const int* rowkappa;
   double2* scratch;
+  double2* Sio;  // partial CP rank sums between pass-B chunks, [row block][E][128]
   long long L;
   int d, K, K_rows, C, kind, Rmax;
+  int p0, p1;        // column pairs of this launch
+  int first, last;   // chunk flags: start the rank sum at zero / finish the rows
+  int nrb;           // row blocks (CTAs loop over them)
   int ranks[MAXD + 1];
 };
 
@@ -472,138 +483,147 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   const int tid = threadIdx.x;
   const int rl8 = tid & 7, t = (tid >> 3) % T, sub = (tid >> 3) / T;
   const int rloc = sub * 8 + rl8;
-  const int rho = blockIdx.x * ROWS + rloc;
-  const bool valid = rho < a.K_rows;
   double2* stP = smem;
   double2* stM = smem + STG;
   double2* Sb = smem + 2 * STG;  // CP rank sum, [k2][row] (conflict-free across the rows of a warp)
   const size_t plane = (size_t)a.K_rows * N2;
-  const double2* Tb = a.T + (valid ? rho : 0);  // + pair*2*plane + {0, plane} + n2*K_rows
-  auto fetch = [&](double2* stage, int p, int pl) {
-    const double2* src = Tb + ((size_t)p * 2 + pl) * plane;
-#pragma unroll
-    for (int i = 0; i < E; ++i) cp_async16(stage + i * 128 + tid, src + (size_t)(t + T * i) * a.K_rows, valid);
-    cp_async_commit();
-  };
-  cplx S[E], acc[E];
-#pragma unroll
-  for (int i = 0; i < E; ++i) {
-    S[i] = mk(0.0, 0.0);
-    acc[i] = mk(0.0, 0.0);
-  }
   const int d = a.d;
   const int C = a.C;
-  const int npairs = (C + 1) / 2;
-  if constexpr (!TT) {
-#pragma unroll
-    for (int i = 0; i < E; ++i) Sb[(t + T * i) * ROWS + rloc] = make_double2(0.0, 0.0);
-  }
-  // TT: fiber c -> (core lam, rn, rp), tracked incrementally
-  int lam = 0, rn = 0, rp = 0;
+  // TT: per-CTA chain scratch (reused by every row block of this CTA)
   const size_t slot = (size_t)blockIdx.x * 2 * a.Rmax;
   auto st = [&](int b, int r, int i) -> double2* {
     return a.scratch + ((slot + (size_t)b * a.Rmax + r) * E + i) * blockDim.x + tid;
   };
 
-  auto process = [&](cplx (&X)[E], int c) {
+  for (int rb = blockIdx.x; rb < a.nrb; rb += gridDim.x) {
+    const int rho = rb * ROWS + rloc;
+    const bool valid = rho < a.K_rows;
+    const double2* Tb = a.T + (valid ? rho : 0);  // + pair*2*plane + {0, plane} + n2*K_rows
+    auto fetch = [&](double2* stage, int p, int pl) {
+      const double2* src = Tb + ((size_t)p * 2 + pl) * plane;
+#pragma unroll
+      for (int i = 0; i < E; ++i) cp_async16(stage + i * 128 + tid, src + (size_t)(t + T * i) * a.K_rows, valid);
+      cp_async_commit();
+    };
+    cplx S[E], acc[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      S[i] = mk(0.0, 0.0);
+      acc[i] = mk(0.0, 0.0);
+    }
+    double2* Sio = a.Sio ? a.Sio + (size_t)rb * E * 128 + tid : nullptr;
     if constexpr (!TT) {
-      const int m = c % d;  // rank-major columns: c = r d + m
-      if (m == 0) {
 #pragma unroll
-        for (int i = 0; i < E; ++i) acc[i] = X[i];
-      } else {
+      for (int i = 0; i < E; ++i) Sb[(t + T * i) * ROWS + rloc] = a.first ? make_double2(0.0, 0.0) : Sio[i * 128];
+    }
+    // TT: fiber c -> (core lam, rn, rp), tracked incrementally
+    int lam = 0, rn = 0, rp = 0;
+
+    auto process = [&](cplx (&X)[E], int c) {
+      if constexpr (!TT) {
+        const int m = c % d;  // rank-major columns: c = r d + m
+        if (m == 0) {
 #pragma unroll
-        for (int i = 0; i < E; ++i) acc[i] = cmul(acc[i], X[i]);
-      }
-      if (m == d - 1) {
+          for (int i = 0; i < E; ++i) acc[i] = X[i];
+        } else {
 #pragma unroll
-        for (int i = 0; i < E; ++i) {
-          double2* sp = Sb + (t + T * i) * ROWS + rloc;
-          sts_c(sp, cadd(lds_c(sp), acc[i]));
+          for (int i = 0; i < E; ++i) acc[i] = cmul(acc[i], X[i]);
         }
-      }
-    } else {
-      const int rp_n = a.ranks[lam];
-      if (lam == 0) {
+        if (m == d - 1) {
 #pragma unroll
-        for (int i = 0; i < E; ++i) sts_c(st(0, rn, i), X[i]);
-      } else {
-        if (rp == 0) {
-#pragma unroll
-          for (int i = 0; i < E; ++i) acc[i] = mk(0.0, 0.0);
+          for (int i = 0; i < E; ++i) {
+            double2* sp = Sb + (t + T * i) * ROWS + rloc;
+            sts_c(sp, cadd(lds_c(sp), acc[i]));
+          }
         }
+      } else {
+        const int rp_n = a.ranks[lam];
+        if (lam == 0) {
 #pragma unroll
-        for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(lds_c(st((lam - 1) & 1, rp, i)), X[i]));
-        if (rp == rp_n - 1) {
-          if (lam == d - 1) {
+          for (int i = 0; i < E; ++i) sts_c(st(0, rn, i), X[i]);
+        } else {
+          if (rp == 0) {
 #pragma unroll
-            for (int i = 0; i < E; ++i) S[i] = acc[i];
-          } else {
+            for (int i = 0; i < E; ++i) acc[i] = mk(0.0, 0.0);
+          }
 #pragma unroll
-            for (int i = 0; i < E; ++i) sts_c(st(lam & 1, rn, i), acc[i]);
+          for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(lds_c(st((lam - 1) & 1, rp, i)), X[i]));
+          if (rp == rp_n - 1) {
+            if (lam == d - 1) {
+#pragma unroll
+              for (int i = 0; i < E; ++i) S[i] = acc[i];
+            } else {
+#pragma unroll
+              for (int i = 0; i < E; ++i) sts_c(st(lam & 1, rn, i), acc[i]);
+            }
+          }
+        }
+        // advance (lam, rn, rp) in fiber order: rn-major, rp inner
+        if (++rp == rp_n) {
+          rp = 0;
+          if (++rn == a.ranks[lam + 1]) {
+            rn = 0;
+            ++lam;
           }
         }
       }
-      // advance (lam, rn, rp) in fiber order: rn-major, rp inner
-      if (++rp == rp_n) {
-        rp = 0;
-        if (++rn == a.ranks[lam + 1]) {
-          rn = 0;
-          ++lam;
-        }
+    };
+
+    fetch(stP, a.p0, 0);
+    fetch(stM, a.p0, 1);
+    for (int p = a.p0; p < a.p1; ++p) {
+      const bool more = p + 1 < a.p1;
+      cplx vp[E], vm[E];
+      cp_async_wait<1>();  // P(p) landed (M(p) may still be in flight)
+#pragma unroll
+      for (int i = 0; i < E; ++i) vp[i] = lds_c(stP + i * 128 + tid);
+      __syncthreads();  // every thread holds its P slots before the stage turns into exchange space
+      fft_fwd<N2>(vp, t, stP + rloc * SE, a.tw);  // ends past its last barrier: stage free again
+      if (more) fetch(stP, p + 1, 0); else cp_async_commit();
+      cp_async_wait<1>();  // M(p) landed
+#pragma unroll
+      for (int i = 0; i < E; ++i) vm[i] = lds_c(stM + i * 128 + tid);
+      __syncthreads();
+      fft_fwd<N2>(vm, t, stM + rloc * SE, a.tw);
+      if (more) fetch(stM, p + 1, 1); else cp_async_commit();
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const cplx P = vp[i];
+        vp[i] = cscale(cadd(P, vm[i]), 0.5);
+        vm[i] = cscale(mul_mi(csub(P, vm[i])), 0.5);
       }
+      process(vp, 2 * p);
+      if (2 * p + 1 < C) process(vm, 2 * p + 1);
     }
-  };
-
-  fetch(stP, 0, 0);
-  fetch(stM, 0, 1);
-  for (int p = 0; p < npairs; ++p) {
-    const bool more = p + 1 < npairs;
-    cplx vp[E], vm[E];
-    cp_async_wait<1>();  // P(p) landed (M(p) may still be in flight)
-#pragma unroll
-    for (int i = 0; i < E; ++i) vp[i] = lds_c(stP + i * 128 + tid);
-    __syncthreads();  // every thread holds its P slots before the stage turns into exchange space
-    fft_fwd<N2>(vp, t, stP + rloc * SE, a.tw);  // ends past its last barrier: stage free again
-    if (more) fetch(stP, p + 1, 0); else cp_async_commit();
-    cp_async_wait<1>();  // M(p) landed
-#pragma unroll
-    for (int i = 0; i < E; ++i) vm[i] = lds_c(stM + i * 128 + tid);
+    cp_async_wait<0>();
     __syncthreads();
-    fft_fwd<N2>(vm, t, stM + rloc * SE, a.tw);
-    if (more) fetch(stM, p + 1, 1); else cp_async_commit();
+    if constexpr (!TT) {
+      if (!a.last) {  // hand the partial rank sum to the next chunk
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const cplx P = vp[i];
-      vp[i] = cscale(cadd(P, vm[i]), 0.5);
-      vm[i] = cscale(mul_mi(csub(P, vm[i])), 0.5);
+        for (int i = 0; i < E; ++i) Sio[i * 128] = Sb[(t + T * i) * ROWS + rloc];
+        continue;
+      }
+#pragma unroll
+      for (int i = 0; i < E; ++i) S[i] = lds_c(Sb + (t + T * i) * ROWS + rloc);
     }
-    process(vp, 2 * p);
-    if (2 * p + 1 < C) process(vm, 2 * p + 1);
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  if constexpr (!TT) {
-#pragma unroll
-    for (int i = 0; i < E; ++i) S[i] = lds_c(Sb + (t + T * i) * ROWS + rloc);
-  }
 
-  // (d-1)-position shift (s'[t] = s[t-(d-1)] <=> S'[k] = S[k] W_L^{(d-1)k}), inverse row FFT, inverse twiddle, Hermitian weight
-  const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
-#pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const long long k = (long long)kap + (long long)a.K * (t + T * i);
-    const long long m = ((long long)(d - 1) * k) % a.L;
-    S[i] = cmul(S[i], twL(a.tabLlo, a.tabLhi, m));  // shift by d-1: * W_L^{+(d-1)k}
-  }
-  fft_inv<N2>(S, t, stP + rloc * SE, a.tw);
-  const double wgt = (kap == 0 || 2 * kap == a.K) ? 1.0 : 2.0;
-  if (valid) {
+    // (d-1)-position shift (s'[t] = s[t-(d-1)] <=> S'[k] = S[k] W_L^{(d-1)k}), inverse row FFT, inverse twiddle, Hermitian weight
+    const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
 #pragma unroll
     for (int i = 0; i < E; ++i) {
-      const int n2 = t + T * i;
-      const cplx u = cscale(cmulc(S[i], twL(a.tabLlo, a.tabLhi, (long long)n2 * kap)), wgt);
-      sts_c(a.U + (size_t)n2 * a.K_rows + rho, u);
+      const long long k = (long long)kap + (long long)a.K * (t + T * i);
+      const long long m = ((long long)(d - 1) * k) % a.L;
+      S[i] = cmul(S[i], twL(a.tabLlo, a.tabLhi, m));  // shift by d-1: * W_L^{+(d-1)k}
+    }
+    fft_inv<N2>(S, t, stP + rloc * SE, a.tw);
+    const double wgt = (kap == 0 || 2 * kap == a.K) ? 1.0 : 2.0;
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int n2 = t + T * i;
+        const cplx u = cscale(cmulc(S[i], twL(a.tabLlo, a.tabLhi, (long long)n2 * kap)), wgt);
+        sts_c(a.U + (size_t)n2 * a.K_rows + rho, u);
+      }
     }
   }
 }
@@ -1122,13 +1142,17 @@ int dispatchA(int N1, const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
 
 // ---- pass B
 template <int N2, bool TT>
-int launchB(const PassBArgs& a, cudaStream_t st) {
+size_t smemB() {
   constexpr int T = fft_t(N2);
   constexpr int ROWS = 128 / T;
   constexpr size_t STG = std::max((size_t)ROWS * fft_smem_elems(N2), (size_t)fft_e(N2) * 128);
-  const size_t smem = (2 * STG + (size_t)ROWS * N2) * sizeof(double2);
+  return (2 * STG + (size_t)ROWS * N2) * sizeof(double2);
+}
+
+template <int N2, bool TT>
+int launchB(const PassBArgs& a, int grid, cudaStream_t st) {
+  const size_t smem = smemB<N2, TT>();
   TRY(set_smem(passB_kernel<N2, TT>, smem));
-  const int grid = (a.K_rows + ROWS - 1) / ROWS;
   passB_kernel<N2, TT><<<grid, 128, smem, st>>>(a);
   CUDA_TRY(cudaGetLastError());
   return TTAGG_OK;
@@ -1136,9 +1160,9 @@ int launchB(const PassBArgs& a, cudaStream_t st) {
 
 int rowsB(int N2) { return 128 / fft_t(N2); }
 
-int dispatchB(int N2, bool tt, const PassBArgs& a, cudaStream_t st) {
+int dispatchB(int N2, bool tt, const PassBArgs& a, int grid, cudaStream_t st) {
 #define TTAGG_B(n) \
-  case n: return tt ? launchB<n, true>(a, st) : launchB<n, false>(a, st);
+  case n: return tt ? launchB<n, true>(a, grid, st) : launchB<n, false>(a, grid, st);
   switch (N2) {
     TTAGG_B(16)
     TTAGG_B(32)
@@ -1212,6 +1236,25 @@ struct ProfScope {
   }
 };
 
+// A/B chunk pipeline knobs (TTAGG_PIPE_CHUNKS, TTAGG_PIPE_BGRID: pass-B CTAs
+// per pipelined launch, 0 = one per row block; default one per SM)
+int pipe_chunks() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TTAGG_PIPE_CHUNKS");
+    v = e ? std::max(1, atoi(e)) : 1;
+  }
+  return v;
+}
+int pipe_bgrid(ttagg_ctx* ctx) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("TTAGG_PIPE_BGRID");
+    v = e ? atoi(e) : -1;
+  }
+  return v >= 0 ? v : ctx->num_sms;
+}
+
 // Evaluate the gain of one kernel into pbuf slot and/or its loss coefficients.
 int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const double* kv, double alpha, bool wantP,
               bool wantQ, double* p_out, ttagg_ctx::Lane& ln, cudaStream_t st) {
@@ -1252,10 +1295,39 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
     a.res_base[j] = P->res_base[j];
     a.res_cnt[j] = P->res_cnt[j];
   }
-  {
+  // A/B chunk pipeline (CP gains): the column pairs split into rank-aligned
+  // chunks; pass A of chunk i+1 runs while pass B of chunk i streams the
+  // exchange rows of chunk i on a second, higher-priority stream, and pass B
+  // carries the partial rank sums from chunk to chunk (Sio).
+  std::vector<int> cut{0, npairs};
+  if (wantP && k->kind == TTAGG_KIND_CP && ln.sB) {
+    const int want = pipe_chunks();
+    const int unit = (k->d % 2) ? k->d : k->d / 2;  // pairs per rank-aligned step
+    if (want > 1 && npairs >= 2 * unit) {
+      cut.assign(1, 0);
+      for (int i = 1; i < want; ++i) {
+        const int b = (int)(((long long)npairs * i / want) / unit * unit);
+        if (b > cut.back() && b < npairs) cut.push_back(b);
+      }
+      cut.push_back(npairs);
+    }
+  }
+  const int nch = (int)cut.size() - 1;
+  cudaStream_t sB = nch > 1 ? ln.sB : st;
+  if (nch > 1) {
+    while ((int)ln.ev.size() < nch) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ln.ev.push_back(e);
+    }
+    if (!ln.evB) CUDA_TRY(cudaEventCreateWithFlags(&ln.evB, cudaEventDisableTiming));
+  }
+  for (int i = 0; i < nch; ++i) {
+    a.pair0 = cut[i];
     ProfScope ps(ctx, 0, st, k->d);
-    TRY(dispatchA(g.N1, a, g.N2, npairs, st));
+    TRY(dispatchA(g.N1, a, g.N2, cut[i + 1] - cut[i], st));
     ++ctx->launches;
+    if (nch > 1) CUDA_TRY(cudaEventRecord(ln.ev[i], st));
   }
   if (wantQ) {
     QArgs q{};
@@ -1291,16 +1363,28 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
     b.kind = k->kind;
     b.Rmax = k->Rmax;
     for (int i = 0; i <= MAXD; ++i) b.ranks[i] = k->ranks[i];
+    const int rows = rowsB(g.N2);
+    b.nrb = (P->K_rows + rows - 1) / rows;
+    int gridB = b.nrb;
     if (k->kind == TTAGG_KIND_TT) {
-      const int rows = rowsB(g.N2);
-      const int grid = (P->K_rows + rows - 1) / rows;
-      const size_t need = (size_t)grid * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
+      const size_t need = (size_t)gridB * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
       TRY(ensure((void**)&ln.scratch, &ln.scratch_bytes, need));
       b.scratch = ln.scratch;
     }
-    {
-      ProfScope ps(ctx, 1, st, k->d);
-      TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, st));
+    if (nch > 1) {
+      TRY(ensure((void**)&ln.Sio, &ln.Sio_bytes, (size_t)b.nrb * fft_e(g.N2) * 128 * sizeof(double2)));
+      b.Sio = ln.Sio;
+      const int pg = pipe_bgrid(ctx);
+      if (pg > 0) gridB = std::min(gridB, pg);
+    }
+    for (int i = 0; i < nch; ++i) {
+      b.p0 = cut[i];
+      b.p1 = cut[i + 1];
+      b.first = i == 0;
+      b.last = i == nch - 1;
+      if (nch > 1) CUDA_TRY(cudaStreamWaitEvent(sB, ln.ev[i], 0));
+      ProfScope ps(ctx, 1, sB, k->d);
+      TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, gridB, sB));
       ++ctx->launches;
     }
     PassCArgs c{};
@@ -1321,9 +1405,15 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       c.res_base[j] = P->res_base[j];
       c.res_cnt[j] = P->res_cnt[j];
     }
-    ProfScope ps(ctx, 2, st, k->d);
-    TRY(dispatchC(g.N1, c, g.N2, st));
-    ++ctx->launches;
+    {
+      ProfScope ps(ctx, 2, sB, k->d);
+      TRY(dispatchC(g.N1, c, g.N2, sB));
+      ++ctx->launches;
+    }
+    if (nch > 1) {
+      CUDA_TRY(cudaEventRecord(ln.evB, sB));
+      CUDA_TRY(cudaStreamWaitEvent(st, ln.evB, 0));
+    }
   }
   return TTAGG_OK;
 }
@@ -1348,8 +1438,12 @@ int make_lanes(ttagg_ctx* ctx) {
   CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   // lane 0 (the most expensive order) at the greatest priority, lane 1 at the least:
   // lane-1 blocks fill the SMs that lane 0's last wave leaves idle
-  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[0].s, cudaStreamNonBlocking, hi));
+  const int mid = (lo + hi) / 2;
+  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[0].s, cudaStreamNonBlocking, mid));
+  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[0].sB, cudaStreamNonBlocking, hi));
   CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[1].s, cudaStreamNonBlocking, lo));
+  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[1].sB, cudaStreamNonBlocking, lo));
+  CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   for (auto& ln : ctx->lane) CUDA_TRY(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   return TTAGG_OK;
@@ -1367,8 +1461,8 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
   int big = 0;
   for (int i = 1; i < nk; ++i)
     if (order_cost(ks[i]) > order_cost(ks[big])) big = i;
+  if (wantP) TRY(make_lanes(ctx));
   if (conc) {
-    TRY(make_lanes(ctx));
     CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
     for (auto& ln : ctx->lane) CUDA_TRY(cudaStreamWaitEvent(ln.s, ctx->ev_fork, 0));
   }
@@ -1477,8 +1571,12 @@ int ttagg_ctx_destroy(ttagg_ctx* ctx) {
     cudaFree(ln.T);
     cudaFree(ln.U);
     cudaFree(ln.scratch);
+    cudaFree(ln.Sio);
     if (ln.s) cudaStreamDestroy(ln.s);
+    if (ln.sB) cudaStreamDestroy(ln.sB);
     if (ln.done) cudaEventDestroy(ln.done);
+    if (ln.evB) cudaEventDestroy(ln.evB);
+    for (auto e : ln.ev) cudaEventDestroy(e);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   cudaFree(ctx->pbuf);
