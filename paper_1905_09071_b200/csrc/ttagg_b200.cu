@@ -60,6 +60,7 @@ constexpr int LLO = 1 << LSPLIT;
 // residue row blocks are padded to multiples of RB rows (8 x 16 B: every n2 row of the
 // exchange starts on a 128-byte line, so pass B's 8-row warp loads are whole lines)
 constexpr int RB = TTAGG_RB;
+constexpr int OFS_N = 22;  // per-row constants of fft_fwd_rowoff (16 first-stage + 3 x 2 inner)
 
 thread_local std::string g_err;
 
@@ -142,25 +143,18 @@ struct ttagg_ctx {
   std::mutex mu;
   double2* tw4096 = nullptr;
   std::map<std::pair<int, int64_t>, OrderPlan*> plans;
-  // workspaces: one lane per concurrently running order chain (exchange T,
-  // inverse rows U, TT chain scratch) on its own stream
-  struct Lane {
+  // workspaces: one per order slot of a kernel set (exchange T, inverse rows U,
+  // TT chain scratch), so the orders' passes can run concurrently
+  struct Work {
     double2* T = nullptr;
     size_t T_bytes = 0;
     double2* U = nullptr;
     size_t U_bytes = 0;
     double2* scratch = nullptr;
     size_t scratch_bytes = 0;
-    double2* Sio = nullptr;  // partial rank sums between pass-B chunks
-    size_t Sio_bytes = 0;
-    cudaStream_t s = nullptr;
-    cudaStream_t sB = nullptr;  // pass-B stream of the A/B chunk pipeline
-    cudaEvent_t done = nullptr;
-    std::vector<cudaEvent_t> ev;  // per-chunk pass-A completion
-    cudaEvent_t evB = nullptr;
-  } lane[2];
-  int num_sms = 0;
-  cudaEvent_t ev_fork = nullptr;
+  } work[MAXORD];
+  cudaStream_t s_main = nullptr, s_fill = nullptr;  // mid / least priority
+  cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_fill = nullptr;
   double* pbuf = nullptr;
   size_t pbuf_bytes = 0;
   double* vec = nullptr;  // general vectors (natural/perm state, outputs)
@@ -253,19 +247,26 @@ struct PMOut {
   cplx cn2;     // W_L^(n2 K) = W_N2^(n2)
 };
 
+#ifndef TTAGG_TW_IN_B
+#define TTAGG_TW_IN_B 0
+#endif
+// With TTAGG_TW_IN_B the four-step twiddle W_L^(n2 kappa) is left to pass B
+// (both planes of row kappa take the same factor there), and pass A stores the
+// raw column outputs: P[kappa] = Zcol[kappa], M[K - kappa] = conj(Zcol[kappa]).
 __device__ __forceinline__ void emit_pm(const PassAArgs& a, const PMOut& o, int N1, int d, int j, int k1, cplx Y,
                                         cplx w) {
   if (a.dbg & 1) return;
-  const cplx Yw = cmul(Y, w);
+  const cplx Yw = TTAGG_TW_IN_B ? Y : cmul(Y, w);
+  const cplx Mv = TTAGG_TW_IN_B ? cconj(Y) : cmul(cconj(Yw), o.cn2);
   if (k1 < a.res_cnt[j]) sts_c(o.TP + a.res_base[j] + k1, Yw);
   if (j == 0) {
     if (k1 == 0) {
       sts_c(o.TM + a.res_base[0], cconj(Y));
     } else if (2 * k1 >= N1) {
-      sts_c(o.TM + a.res_base[0] + (N1 - k1), cmul(cconj(Yw), o.cn2));
+      sts_c(o.TM + a.res_base[0] + (N1 - k1), Mv);
     }
   } else if (2 * k1 >= N1) {
-    sts_c(o.TM + a.res_base[d - j] + (N1 - 1 - k1), cmul(cconj(Yw), o.cn2));
+    sts_c(o.TM + a.res_base[d - j] + (N1 - 1 - k1), Mv);
   }
 }
 
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   double2* stP = smem;
   double2* stM = smem + STG;
   double2* Sb = smem + 2 * STG;  // CP rank sum, [k2][row] (conflict-free across the rows of a warp)
+  double2* Ost = Sb + ROWS * N2;  // [k][row]: offset constants of fft_fwd_rowoff (four-step twiddle)
   const size_t plane = (size_t)a.K_rows * N2;
   const int d = a.d;
   const int C = a.C;
@@ -518,6 +520,33 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     }
     // TT: fiber c -> (core lam, rn, rp), tracked incrementally
     int lam = 0, rn = 0, rp = 0;
+#if TTAGG_TW_IN_B
+    // the four-step twiddle W_L^(n2 kappa) of this row = a frequency offset of
+    // kappa/K in the row transforms: per-row stage constants (L = K N2)
+    {
+      const long long kap0 = valid ? max(a.rowkappa[rho], 0) : 0;
+      constexpr int b = fft_first_radix(N2) > 1 ? fft_first_radix(N2) : 16;
+      for (int k = t; k < OFS_N; k += T) {
+        long long ex = 0;
+        if (k < 16) {
+          if (k < b) ex = kap0 * k * (N2 / b);
+        } else {
+          const int s2 = (k - 16) >> 1, NS = b << (4 * s2);
+          ex = 16 * NS <= N2 ? ((k & 1) ? 4 : 1) * kap0 * (N2 / (16 * NS)) : 0;
+        }
+        const cplx w = twL(a.tabLlo, a.tabLhi, ex % a.L);
+        Ost[k * ROWS + rloc] = make_double2(w.x, w.y);
+      }
+    }
+#endif
+
+    auto row_fft = [&](cplx (&v)[E], double2* stage) {
+#if TTAGG_TW_IN_B
+      fft_fwd_rowoff<N2>(v, t, stage + rloc * SE, a.tw, Ost + rloc, ROWS);
+#else
+      fft_fwd<N2>(v, t, stage + rloc * SE, a.tw);
+#endif
+    };
 
     auto process = [&](cplx (&X)[E], int c) {
       if constexpr (!TT) {
@@ -578,13 +607,13 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
 #pragma unroll
       for (int i = 0; i < E; ++i) vp[i] = lds_c(stP + i * 128 + tid);
       __syncthreads();  // every thread holds its P slots before the stage turns into exchange space
-      fft_fwd<N2>(vp, t, stP + rloc * SE, a.tw);  // ends past its last barrier: stage free again
+      row_fft(vp, stP);  // ends past its last barrier: stage free again
       if (more) fetch(stP, p + 1, 0); else cp_async_commit();
       cp_async_wait<1>();  // M(p) landed
 #pragma unroll
       for (int i = 0; i < E; ++i) vm[i] = lds_c(stM + i * 128 + tid);
       __syncthreads();
-      fft_fwd<N2>(vm, t, stM + rloc * SE, a.tw);
+      row_fft(vm, stM);
       if (more) fetch(stM, p + 1, 1); else cp_async_commit();
 #pragma unroll
       for (int i = 0; i < E; ++i) {
@@ -1146,7 +1175,7 @@ size_t smemB() {
   constexpr int T = fft_t(N2);
   constexpr int ROWS = 128 / T;
   constexpr size_t STG = std::max((size_t)ROWS * fft_smem_elems(N2), (size_t)fft_e(N2) * 128);
-  return (2 * STG + (size_t)ROWS * N2) * sizeof(double2);
+  return (2 * STG + (size_t)ROWS * N2 + (size_t)ROWS * OFS_N) * sizeof(double2);
 }
 
 template <int N2, bool TT>
@@ -1236,43 +1265,24 @@ struct ProfScope {
   }
 };
 
-// A/B chunk pipeline knobs (TTAGG_PIPE_CHUNKS, TTAGG_PIPE_BGRID: pass-B CTAs
-// per pipelined launch, 0 = one per row block; default one per SM)
-int pipe_chunks() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TTAGG_PIPE_CHUNKS");
-    v = e ? std::max(1, atoi(e)) : 1;
-  }
-  return v;
-}
-int pipe_bgrid(ttagg_ctx* ctx) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("TTAGG_PIPE_BGRID");
-    v = e ? atoi(e) : -1;
-  }
-  return v >= 0 ? v : ctx->num_sms;
-}
-
-// Evaluate the gain of one kernel into pbuf slot and/or its loss coefficients.
-int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const double* kv, double alpha, bool wantP,
-              bool wantQ, double* p_out, ttagg_ctx::Lane& ln, cudaStream_t st) {
+// Pass A (column transforms + loss column sums) and qcoef of one order.
+int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const double* kv, double alpha, bool wantP,
+              bool wantQ, ttagg_ctx::Work& w, cudaStream_t st) {
   const OrderPlan* P = k->plan;
   const Geom& g = k->g;
   const int npairs = k->C_pad / 2;
   if (npairs > 65535) return fail(TTAGG_ERR_UNSUPPORTED, "too many columns for one kernel");
   if (wantP) {
     const size_t need = (size_t)k->C_pad * P->K_rows * g.N2 * sizeof(double2);
-    TRY(ensure((void**)&ln.T, &ln.T_bytes, need, true));
-    TRY(ensure((void**)&ln.U, &ln.U_bytes, (size_t)P->K_rows * g.N2 * sizeof(double2)));
+    TRY(ensure((void**)&w.T, &w.T_bytes, need, true));
+    TRY(ensure((void**)&w.U, &w.U_bytes, (size_t)P->K_rows * g.N2 * sizeof(double2)));
   }
   PassAArgs a{};
   a.X = k->X;
   a.nv = nv;
   a.kv = kv;
   a.alpha = alpha;
-  a.T = ln.T;
+  a.T = w.T;
   a.dots = k->dots;
   a.tw = ctx->tw4096;
   a.tabK = P->tabK;
@@ -1283,6 +1293,7 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
   a.K_rows = P->K_rows;
   a.nblk = k->nblk;
   a.want_T = wantP ? 1 : 0;
+  a.pair0 = 0;
   {
     static int dbg = -1;
     if (dbg < 0) {
@@ -1295,39 +1306,10 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
     a.res_base[j] = P->res_base[j];
     a.res_cnt[j] = P->res_cnt[j];
   }
-  // A/B chunk pipeline (CP gains): the column pairs split into rank-aligned
-  // chunks; pass A of chunk i+1 runs while pass B of chunk i streams the
-  // exchange rows of chunk i on a second, higher-priority stream, and pass B
-  // carries the partial rank sums from chunk to chunk (Sio).
-  std::vector<int> cut{0, npairs};
-  if (wantP && k->kind == TTAGG_KIND_CP && ln.sB) {
-    const int want = pipe_chunks();
-    const int unit = (k->d % 2) ? k->d : k->d / 2;  // pairs per rank-aligned step
-    if (want > 1 && npairs >= 2 * unit) {
-      cut.assign(1, 0);
-      for (int i = 1; i < want; ++i) {
-        const int b = (int)(((long long)npairs * i / want) / unit * unit);
-        if (b > cut.back() && b < npairs) cut.push_back(b);
-      }
-      cut.push_back(npairs);
-    }
-  }
-  const int nch = (int)cut.size() - 1;
-  cudaStream_t sB = nch > 1 ? ln.sB : st;
-  if (nch > 1) {
-    while ((int)ln.ev.size() < nch) {
-      cudaEvent_t e;
-      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      ln.ev.push_back(e);
-    }
-    if (!ln.evB) CUDA_TRY(cudaEventCreateWithFlags(&ln.evB, cudaEventDisableTiming));
-  }
-  for (int i = 0; i < nch; ++i) {
-    a.pair0 = cut[i];
+  {
     ProfScope ps(ctx, 0, st, k->d);
-    TRY(dispatchA(g.N1, a, g.N2, cut[i + 1] - cut[i], st));
+    TRY(dispatchA(g.N1, a, g.N2, npairs, st));
     ++ctx->launches;
-    if (nch > 1) CUDA_TRY(cudaEventRecord(ln.ev[i], st));
   }
   if (wantQ) {
     QArgs q{};
@@ -1347,74 +1329,65 @@ int run_order(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
     CUDA_TRY(cudaGetLastError());
     ++ctx->launches;
   }
-  if (wantP) {
-    PassBArgs b{};
-    b.T = ln.T;
-    b.U = ln.U;
-    b.tw = ctx->tw4096;
-    b.tabLlo = P->tabLlo;
-    b.tabLhi = P->tabLhi;
-    b.rowkappa = P->rowkappa;
-    b.L = P->L;
-    b.d = k->d;
-    b.K = P->K;
-    b.K_rows = P->K_rows;
-    b.C = k->C;
-    b.kind = k->kind;
-    b.Rmax = k->Rmax;
-    for (int i = 0; i <= MAXD; ++i) b.ranks[i] = k->ranks[i];
-    const int rows = rowsB(g.N2);
-    b.nrb = (P->K_rows + rows - 1) / rows;
-    int gridB = b.nrb;
-    if (k->kind == TTAGG_KIND_TT) {
-      const size_t need = (size_t)gridB * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
-      TRY(ensure((void**)&ln.scratch, &ln.scratch_bytes, need));
-      b.scratch = ln.scratch;
-    }
-    if (nch > 1) {
-      TRY(ensure((void**)&ln.Sio, &ln.Sio_bytes, (size_t)b.nrb * fft_e(g.N2) * 128 * sizeof(double2)));
-      b.Sio = ln.Sio;
-      const int pg = pipe_bgrid(ctx);
-      if (pg > 0) gridB = std::min(gridB, pg);
-    }
-    for (int i = 0; i < nch; ++i) {
-      b.p0 = cut[i];
-      b.p1 = cut[i + 1];
-      b.first = i == 0;
-      b.last = i == nch - 1;
-      if (nch > 1) CUDA_TRY(cudaStreamWaitEvent(sB, ln.ev[i], 0));
-      ProfScope ps(ctx, 1, sB, k->d);
-      TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, gridB, sB));
-      ++ctx->launches;
-    }
-    PassCArgs c{};
-    c.U = ln.U;
-    c.p = p_out;
-    c.tw = ctx->tw4096;
-    c.tabK = P->tabK;
-    c.N = g.N;
-    c.invL = 1.0 / (double)P->L;
-    double f = 1.0;
-    for (int i = 2; i <= k->d; ++i) f *= i;
-    c.fact = f;
-    c.d = k->d;
-    c.N2 = g.N2;
-    c.K_rows = P->K_rows;
-    c.nres = P->nres;
-    for (int j = 0; j < MAXRES; ++j) {
-      c.res_base[j] = P->res_base[j];
-      c.res_cnt[j] = P->res_cnt[j];
-    }
-    {
-      ProfScope ps(ctx, 2, sB, k->d);
-      TRY(dispatchC(g.N1, c, g.N2, sB));
-      ++ctx->launches;
-    }
-    if (nch > 1) {
-      CUDA_TRY(cudaEventRecord(ln.evB, sB));
-      CUDA_TRY(cudaStreamWaitEvent(st, ln.evB, 0));
-    }
+  return TTAGG_OK;
+}
+
+// Pass B (row transforms, spectral product/chain) and pass C of one order.
+int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::Work& w, cudaStream_t st) {
+  const OrderPlan* P = k->plan;
+  const Geom& g = k->g;
+  PassBArgs b{};
+  b.T = w.T;
+  b.U = w.U;
+  b.tw = ctx->tw4096;
+  b.tabLlo = P->tabLlo;
+  b.tabLhi = P->tabLhi;
+  b.rowkappa = P->rowkappa;
+  b.L = P->L;
+  b.d = k->d;
+  b.K = P->K;
+  b.K_rows = P->K_rows;
+  b.C = k->C;
+  b.kind = k->kind;
+  b.Rmax = k->Rmax;
+  for (int i = 0; i <= MAXD; ++i) b.ranks[i] = k->ranks[i];
+  const int rows = rowsB(g.N2);
+  b.nrb = (P->K_rows + rows - 1) / rows;
+  b.p0 = 0;
+  b.p1 = k->C_pad / 2;
+  b.first = b.last = 1;
+  b.Sio = nullptr;
+  if (k->kind == TTAGG_KIND_TT) {
+    const size_t need = (size_t)b.nrb * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
+    TRY(ensure((void**)&w.scratch, &w.scratch_bytes, need));
+    b.scratch = w.scratch;
   }
+  {
+    ProfScope ps(ctx, 1, st, k->d);
+    TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, b.nrb, st));
+    ++ctx->launches;
+  }
+  PassCArgs c{};
+  c.U = w.U;
+  c.p = p_out;
+  c.tw = ctx->tw4096;
+  c.tabK = P->tabK;
+  c.N = g.N;
+  c.invL = 1.0 / (double)P->L;
+  double f = 1.0;
+  for (int i = 2; i <= k->d; ++i) f *= i;
+  c.fact = f;
+  c.d = k->d;
+  c.N2 = g.N2;
+  c.K_rows = P->K_rows;
+  c.nres = P->nres;
+  for (int j = 0; j < MAXRES; ++j) {
+    c.res_base[j] = P->res_base[j];
+    c.res_cnt[j] = P->res_cnt[j];
+  }
+  ProfScope ps(ctx, 2, st, k->d);
+  TRY(dispatchC(g.N1, c, g.N2, st));
+  ++ctx->launches;
   return TTAGG_OK;
 }
 
@@ -1432,51 +1405,60 @@ int check_set(const ttagg_kernel* const* ks, int nk, Geom* g) {
 // Relative device cost of one order's gain (column count x transform length).
 double order_cost(const ttagg_kernel* k) { return (double)std::max(k->C_pad, 1) * k->plan->K_rows; }
 
-int make_lanes(ttagg_ctx* ctx) {
-  if (ctx->lane[0].s) return TTAGG_OK;
+int make_streams(ttagg_ctx* ctx) {
+  if (ctx->s_main) return TTAGG_OK;
   int lo = 0, hi = 0;
   CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  // lane 0 (the most expensive order) at the greatest priority, lane 1 at the least:
-  // lane-1 blocks fill the SMs that lane 0's last wave leaves idle
-  const int mid = (lo + hi) / 2;
-  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[0].s, cudaStreamNonBlocking, mid));
-  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[0].sB, cudaStreamNonBlocking, hi));
-  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[1].s, cudaStreamNonBlocking, lo));
-  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->lane[1].sB, cudaStreamNonBlocking, lo));
-  CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-  for (auto& ln : ctx->lane) CUDA_TRY(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->s_main, cudaStreamNonBlocking, (lo + hi) / 2));
+  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->s_fill, cudaStreamNonBlocking, lo));
+  for (cudaEvent_t* e : {&ctx->ev_fork, &ctx->ev_a, &ctx->ev_fill})
+    CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   return TTAGG_OK;
 }
 
 // Run all orders: gains into pbuf, loss coefficients; fill the combine descriptor.
-// With several orders the most expensive order
-// runs on lane 0 and the others, in decreasing cost, on lane 1; both fork
-// from and join back into `st` (also under stream capture).
+// Several orders: the main stream runs the pass A of every cheaper order, then
+// pass A and pass B/C of the costliest order; the cheaper orders' pass B/C run
+// on a least-priority stream once their pass A is done, so their blocks fill
+// the SMs that the costliest order leaves idle (its last pass-B wave above
+// all).  Both streams fork from and join back into `st` (also under capture).
 int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const double* nv, const double* kv,
                double alpha, bool wantP, bool wantQ, CombineArgs* A, cudaStream_t st) {
   const Geom& g = ks[0]->g;
   if (wantP) TRY(ensure((void**)&ctx->pbuf, &ctx->pbuf_bytes, (size_t)nk * g.Np * sizeof(double)));
-  const bool conc = wantP && nk > 1;
-  int big = 0;
-  for (int i = 1; i < nk; ++i)
-    if (order_cost(ks[i]) > order_cost(ks[big])) big = i;
-  if (wantP) TRY(make_lanes(ctx));
-  if (conc) {
-    CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
-    for (auto& ln : ctx->lane) CUDA_TRY(cudaStreamWaitEvent(ln.s, ctx->ev_fork, 0));
-  }
   std::vector<int> order(nk);
   for (int i = 0; i < nk; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(),
                    [&](int x, int y) { return order_cost(ks[x]) > order_cost(ks[y]); });
-  for (int i : order) {
+  auto pslot = [&](int i) { return wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr; };
+  const bool conc = wantP && nk > 1;
+  if (!conc) {
+    for (int i : order) {
+      TRY(run_passA(ctx, ks[i], nv, kv, alpha, wantP, wantQ, ctx->work[i], st));
+      if (wantP) TRY(run_passBC(ctx, ks[i], pslot(i), ctx->work[i], st));
+    }
+  } else {
+    TRY(make_streams(ctx));
+    const int big = order[0];
+    CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->s_main, ctx->ev_fork, 0));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill, ctx->ev_fork, 0));
+    for (int n = nk - 1; n >= 1; --n)  // cheapest first: their pass B/C can start early
+      TRY(run_passA(ctx, ks[order[n]], nv, kv, alpha, true, wantQ, ctx->work[order[n]], ctx->s_main));
+    CUDA_TRY(cudaEventRecord(ctx->ev_a, ctx->s_main));
+    TRY(run_passA(ctx, ks[big], nv, kv, alpha, true, wantQ, ctx->work[big], ctx->s_main));
+    TRY(run_passBC(ctx, ks[big], pslot(big), ctx->work[big], ctx->s_main));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill, ctx->ev_a, 0));
+    for (int n = 1; n < nk; ++n) TRY(run_passBC(ctx, ks[order[n]], pslot(order[n]), ctx->work[order[n]], ctx->s_fill));
+    CUDA_TRY(cudaEventRecord(ctx->ev_a, ctx->s_main));
+    CUDA_TRY(cudaEventRecord(ctx->ev_fill, ctx->s_fill));
+    CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_a, 0));
+    CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fill, 0));
+  }
+  for (int i = 0; i < nk; ++i) {
     const ttagg_kernel* k = ks[i];
-    double* pslot = wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr;
-    ttagg_ctx::Lane& ln = ctx->lane[conc && i != big ? 1 : 0];
-    TRY(run_order(ctx, k, nv, kv, alpha, wantP, wantQ, pslot, ln, conc ? ln.s : st));
     CombineOrder& o = A->o[i];
-    o.p = pslot;
+    o.p = pslot(i);
     o.X = k->X;
     o.tail = k->tail_cols;
     o.coef = wantQ ? k->coef : nullptr;
@@ -1484,12 +1466,6 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
     double f = 1.0;
     for (int j = 2; j <= k->d - 1; ++j) f *= j;
     o.qdiv = f;
-  }
-  if (conc) {
-    for (auto& ln : ctx->lane) {
-      CUDA_TRY(cudaEventRecord(ln.done, ln.s));
-      CUDA_TRY(cudaStreamWaitEvent(st, ln.done, 0));
-    }
   }
   A->nord = nk;
   A->nv = nv;
@@ -1567,17 +1543,15 @@ int ttagg_ctx_destroy(ttagg_ctx* ctx) {
     delete P;
   }
   cudaFree(ctx->tw4096);
-  for (auto& ln : ctx->lane) {
-    cudaFree(ln.T);
-    cudaFree(ln.U);
-    cudaFree(ln.scratch);
-    cudaFree(ln.Sio);
-    if (ln.s) cudaStreamDestroy(ln.s);
-    if (ln.sB) cudaStreamDestroy(ln.sB);
-    if (ln.done) cudaEventDestroy(ln.done);
-    if (ln.evB) cudaEventDestroy(ln.evB);
-    for (auto e : ln.ev) cudaEventDestroy(e);
+  for (auto& w : ctx->work) {
+    cudaFree(w.T);
+    cudaFree(w.U);
+    cudaFree(w.scratch);
   }
+  for (cudaStream_t x : {ctx->s_main, ctx->s_fill})
+    if (x) cudaStreamDestroy(x);
+  for (cudaEvent_t e : {ctx->ev_a, ctx->ev_fill})
+    if (e) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   cudaFree(ctx->pbuf);
   cudaFree(ctx->vec);
