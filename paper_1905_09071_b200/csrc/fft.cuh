@@ -311,6 +311,25 @@ __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm,
   }
 }
 
+// Two independent forward transforms of length M interleaved stage by stage
+// (twice the independent work between barriers, half the barriers); each has
+// its own exchange buffer.
+template <int M, class Sync = CtaSync>
+__device__ __forceinline__ void fft_fwd2(cplx (&v1)[fft_e(M)], cplx (&v2)[fft_e(M)], int t, double2* sm1, double2* sm2,
+                                         const double2* __restrict__ tw, const Sync& sync = Sync()) {
+  constexpr int b = fft_first_radix(M);
+  constexpr int a = (ilog2c(M) - ilog2c(b)) / 4;
+  static_assert(M >= 256 && b == 1 && a == 2, "two radix-16 stages (M = 256)");
+  fft_stage<M, 16, 1, false>(v1, t, sm1, tw);
+  fft_stage<M, 16, 1, false>(v2, t, sm2, tw);
+  sync();
+  fft_load_regs<M>(v1, t, sm1);
+  fft_load_regs<M>(v2, t, sm2);
+  sync();
+  fft_stage<M, 16, 16, true>(v1, t, sm1, tw);
+  fft_stage<M, 16, 16, true>(v2, t, sm2, tw);
+}
+
 // ---------------------------------------------------------------------------
 // Row transform at a fractional frequency offset:  Y[k] = sum_n x[n] W_M^{n (k + delta)}
 // (= the DFT of x[n] W_M^{n delta}: the four-step twiddle of a pass-B row folded

@@ -250,6 +250,9 @@ struct PMOut {
 #ifndef TTAGG_TW_IN_B
 #define TTAGG_TW_IN_B 0
 #endif
+#ifndef TTAGG_B_JOINT
+#define TTAGG_B_JOINT 1
+#endif
 // With TTAGG_TW_IN_B the four-step twiddle W_L^(n2 kappa) is left to pass B
 // (both planes of row kappa take the same factor there), and pass A stores the
 // raw column outputs: P[kappa] = Zcol[kappa], M[K - kappa] = conj(Zcol[kappa]).
@@ -603,6 +606,26 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     for (int p = a.p0; p < a.p1; ++p) {
       const bool more = p + 1 < a.p1;
       cplx vp[E], vm[E];
+#if TTAGG_B_JOINT
+      if constexpr (N2 == 256 && !TTAGG_TW_IN_B) {
+        cp_async_wait<0>();
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          vp[i] = lds_c(stP + i * 128 + tid);
+          vm[i] = lds_c(stM + i * 128 + tid);
+        }
+        __syncthreads();
+        fft_fwd2<N2>(vp, vm, t, stP + rloc * SE, stM + rloc * SE, a.tw);
+        if (more) {
+          fetch(stP, p + 1, 0);
+          fetch(stM, p + 1, 1);
+        } else {
+          cp_async_commit();
+          cp_async_commit();
+        }
+      } else
+#endif
+      {
       cp_async_wait<1>();  // P(p) landed (M(p) may still be in flight)
 #pragma unroll
       for (int i = 0; i < E; ++i) vp[i] = lds_c(stP + i * 128 + tid);
@@ -615,6 +638,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
       __syncthreads();
       row_fft(vm, stM);
       if (more) fetch(stM, p + 1, 1); else cp_async_commit();
+      }
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const cplx P = vp[i];
