@@ -319,15 +319,35 @@ __device__ __forceinline__ void fft_fwd2(cplx (&v1)[fft_e(M)], cplx (&v2)[fft_e(
                                          const double2* __restrict__ tw, const Sync& sync = Sync()) {
   constexpr int b = fft_first_radix(M);
   constexpr int a = (ilog2c(M) - ilog2c(b)) / 4;
-  static_assert(M >= 256 && b == 1 && a == 2, "two radix-16 stages (M = 256)");
-  fft_stage<M, 16, 1, false>(v1, t, sm1, tw);
-  fft_stage<M, 16, 1, false>(v2, t, sm2, tw);
-  sync();
-  fft_load_regs<M>(v1, t, sm1);
-  fft_load_regs<M>(v2, t, sm2);
-  sync();
-  fft_stage<M, 16, 16, true>(v1, t, sm1, tw);
-  fft_stage<M, 16, 16, true>(v2, t, sm2, tw);
+  static_assert(M >= 256 && a >= 2 && a <= 3, "256 <= M <= 4096");
+  auto xchg = [&]() {
+    sync();
+    fft_load_regs<M>(v1, t, sm1);
+    fft_load_regs<M>(v2, t, sm2);
+    sync();
+  };
+  if constexpr (b > 1) {
+    fft_stage<M, b, 1, false>(v1, t, sm1, tw);
+    fft_stage<M, b, 1, false>(v2, t, sm2, tw);
+    xchg();
+  }
+  constexpr int NS1 = b;
+  if constexpr (a == 2) {
+    fft_stage<M, 16, NS1, false>(v1, t, sm1, tw);
+    fft_stage<M, 16, NS1, false>(v2, t, sm2, tw);
+    xchg();
+    fft_stage<M, 16, NS1 * 16, true>(v1, t, sm1, tw);
+    fft_stage<M, 16, NS1 * 16, true>(v2, t, sm2, tw);
+  } else {
+    fft_stage<M, 16, NS1, false>(v1, t, sm1, tw);
+    fft_stage<M, 16, NS1, false>(v2, t, sm2, tw);
+    xchg();
+    fft_stage<M, 16, NS1 * 16, false>(v1, t, sm1, tw);
+    fft_stage<M, 16, NS1 * 16, false>(v2, t, sm2, tw);
+    xchg();
+    fft_stage<M, 16, NS1 * 256, true>(v1, t, sm1, tw);
+    fft_stage<M, 16, NS1 * 256, true>(v2, t, sm2, tw);
+  }
 }
 
 // ---------------------------------------------------------------------------
