@@ -412,7 +412,7 @@ def main():
                       "achieved_GBs": rhs_gbs, "frac_of_peak": rhs_gbs / peak,
                       "fp64_TFLOPs": fp64_flops(N, cols) / (ms_step * 1e-3) / 1e12},
         "kernel_ms_per_step": breakdown,
-        "kernel_ms_note": "CUDA-event intervals on each launch stream (A/B/C = pass, O = qcoef/combine); the costliest order runs on a high-priority stream, the others on a low-priority one that fills its idle SMs, so their intervals overlap it",
+        "kernel_ms_note": "CUDA-event intervals on each launch stream (A/B/C = pass, O = qcoef/combine); the cheaper orders' pass B/C sit on a least-priority stream that only gets SMs the costliest order leaves idle, so their intervals span that wait",
         "cpu_baseline": cpu,
         "e2e": e2e,
         "rk2": rk2,

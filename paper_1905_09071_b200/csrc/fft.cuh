@@ -43,6 +43,8 @@ __device__ __forceinline__ cplx lds_c(const double2* p) {
   return cplx{v.x, v.y};
 }
 __device__ __forceinline__ void sts_c(double2* p, cplx v) { *p = make_double2(v.x, v.y); }
+// streaming (evict-first) global store: data written once and read by a later kernel
+__device__ __forceinline__ void stg_cs(double2* p, cplx v) { __stcs(p, make_double2(v.x, v.y)); }
 
 // ---------------------------------------------------------------------------
 // small DFTs (forward, W = exp(-2 pi i / R)), in place on v[0..R)

@@ -250,6 +250,14 @@ struct PMOut {
 #ifndef TTAGG_TW_IN_B
 #define TTAGG_TW_IN_B 0
 #endif
+#ifndef TTAGG_EX_CS
+#define TTAGG_EX_CS 1
+#endif
+#if TTAGG_EX_CS
+#define EXST stg_cs
+#else
+#define EXST sts_c
+#endif
 #ifndef TTAGG_B_JOINT
 #define TTAGG_B_JOINT 1
 #endif
@@ -261,15 +269,15 @@ __device__ __forceinline__ void emit_pm(const PassAArgs& a, const PMOut& o, int 
   if (a.dbg & 1) return;
   const cplx Yw = TTAGG_TW_IN_B ? Y : cmul(Y, w);
   const cplx Mv = TTAGG_TW_IN_B ? cconj(Y) : cmul(cconj(Yw), o.cn2);
-  if (k1 < a.res_cnt[j]) sts_c(o.TP + a.res_base[j] + k1, Yw);
+  if (k1 < a.res_cnt[j]) EXST(o.TP + a.res_base[j] + k1, Yw);
   if (j == 0) {
     if (k1 == 0) {
-      sts_c(o.TM + a.res_base[0], cconj(Y));
+      EXST(o.TM + a.res_base[0], cconj(Y));
     } else if (2 * k1 >= N1) {
-      sts_c(o.TM + a.res_base[0] + (N1 - k1), Mv);
+      EXST(o.TM + a.res_base[0] + (N1 - k1), Mv);
     }
   } else if (2 * k1 >= N1) {
-    sts_c(o.TM + a.res_base[d - j] + (N1 - 1 - k1), Mv);
+    EXST(o.TM + a.res_base[d - j] + (N1 - 1 - k1), Mv);
   }
 }
 
