@@ -155,6 +155,7 @@ struct ttagg_ctx {
   } work[MAXORD];
   cudaStream_t s_main = nullptr, s_fill = nullptr;  // mid / least priority
   cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_fill = nullptr;
+  int num_sms = 0;
   double* pbuf = nullptr;
   size_t pbuf_bytes = 0;
   double* vec = nullptr;  // general vectors (natural/perm state, outputs)
@@ -1389,14 +1390,25 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
   b.p1 = k->C_pad / 2;
   b.first = b.last = 1;
   b.Sio = nullptr;
+  int gridB = b.nrb;
   if (k->kind == TTAGG_KIND_TT) {
-    const size_t need = (size_t)b.nrb * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
+    // The chain state (2 Rmax spectra per frequency) lives in a per-CTA global
+    // scratch.  TTAGG_TT_CTAS_PER_SM caps the resident CTAs (persistent
+    // row-block loop) so that all scratch fits L2; measured slower at C4 shape
+    // (occupancy matters more), so uncapped by default.
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      const char* e = getenv("TTAGG_TT_CTAS_PER_SM");
+      per_sm = e ? atoi(e) : 0;
+    }
+    if (per_sm > 0 && ctx->num_sms > 0) gridB = std::min(gridB, per_sm * ctx->num_sms);
+    const size_t need = (size_t)gridB * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
     TRY(ensure((void**)&w.scratch, &w.scratch_bytes, need));
     b.scratch = w.scratch;
   }
   {
     ProfScope ps(ctx, 1, st, k->d);
-    TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, b.nrb, st));
+    TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, gridB, st));
     ++ctx->launches;
   }
   PassCArgs c{};
@@ -1552,6 +1564,7 @@ int ttagg_ctx_create(int device, ttagg_ctx** out) {
   CUDA_TRY(cudaSetDevice(device));
   ttagg_ctx* ctx = new ttagg_ctx();
   ctx->device = device;
+  CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
   std::vector<double2> tw;
   host_twiddles(tw, TW_BASE, TW_BASE, 1);
   CUDA_TRY(cudaMalloc(&ctx->tw4096, TW_BASE * sizeof(double2)));
