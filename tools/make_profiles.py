@@ -83,7 +83,7 @@ def launches(path, tag, command):
         agg[lab] = agg.get(lab, 0.0) + v
     lines = [f"ncu --metrics gpu__time_duration.sum --clock-control none; command: {command}",
              "per-launch device time of the last RHS, cold-cache and serialised under ncu: compare SHARES, not absolutes",
-             "(in the timed bench the costliest order runs on a high-priority stream and the others fill its idle SMs)", ""]
+             "(in the timed bench the cheaper orders' pass B/C run on a least-priority stream that fills the SMs the costliest order leaves idle)", ""]
     for lab, v in sorted(agg.items(), key=lambda x: -x[1]):
         lines.append(f"{lab:28s} {v / 1e3:10.1f} us   {v / tot * 100:5.1f}%")
     lines += ["", f"{'total':28s} {tot / 1e3:10.1f} us over {len(seg)} launches per RHS", "",
