@@ -352,102 +352,6 @@ __device__ __forceinline__ void fft_fwd2(cplx (&v1)[fft_e(M)], cplx (&v2)[fft_e(
   }
 }
 
-// ---------------------------------------------------------------------------
-// Row transform at a fractional frequency offset:  Y[k] = sum_n x[n] W_M^{n (k + delta)}
-// (= the DFT of x[n] W_M^{n delta}: the four-step twiddle of a pass-B row folded
-// into the stages).  Stage (NS, R) uses W_{NS R}^{i (qm + delta)}: the qm part
-// from the W_4096 table, the offset part from per-row constants `ofs` (stride
-// `os` between entries, so rows sharing a warp read consecutive words):
-//   ofs[i * os], i < R0:       W_{R0}^{i delta} for the first stage (radix R0)
-//   ofs[(16 + 2 s) * os], ofs[(17 + 2 s) * os]:  W_{NS R}^{delta}, W_{NS R}^{4 delta}
-//                               for inner radix-16 stage s = 0, 1, 2 (NS = b 16^s)
-// ---------------------------------------------------------------------------
-template <int M, int R, int NS, bool LAST>
-__device__ __forceinline__ void fft_stage_rowoff(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
-                                                 const double2* ofs, int os) {
-  constexpr int E = fft_e(M);
-  constexpr int T = fft_t(M);
-  constexpr int G = E / R;
-  constexpr int b = fft_first_radix(M) > 1 ? fft_first_radix(M) : 16;
-  constexpr int st = NS == 1 ? -1 : (NS == b ? 0 : (NS == b * 16 ? 1 : 2));
-#pragma unroll
-  for (int u = 0; u < G; ++u) {
-    const int q = t + T * u;
-    cplx x[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) x[i] = v[u + i * G];
-    if constexpr (NS == 1) {
-#pragma unroll
-      for (int i = 1; i < R; ++i) x[i] = cmul(x[i], lds_c(ofs + i * os));
-    } else {
-      static_assert(R == 16, "inner stages are radix 16");
-      const int qm = q & (NS - 1);
-      const int e = qm * (TW_BASE / (NS * R));
-      const cplx w1 = cmul(ld_c(tw + e), lds_c(ofs + (16 + 2 * st) * os));
-      const cplx w4 = cmul(ld_c(tw + 4 * e), lds_c(ofs + (17 + 2 * st) * os));
-      twiddle16(x, w1, w4);
-    }
-    DFT<R>::run(x);
-    if constexpr (LAST) {
-#pragma unroll
-      for (int i = 0; i < R; ++i) v[u + i * G] = x[i];
-    } else {
-      const int base = (q / NS) * NS * R + (q & (NS - 1));
-#pragma unroll
-      for (int i = 0; i < R; ++i) sts_c(sm + pad16(base + i * NS), x[i]);
-    }
-  }
-}
-
-template <int M, class Sync = CtaSync>
-__device__ __forceinline__ void fft_fwd_rowoff(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
-                                               const double2* ofs, int os, const Sync& sync = Sync()) {
-  constexpr int b = fft_first_radix(M);
-  constexpr int a = (ilog2c(M) - ilog2c(b)) / 4;
-  static_assert(M >= 16 && a >= 1 && a <= 3, "16 <= M <= 4096");
-  if constexpr (b > 1) {
-    fft_stage_rowoff<M, b, 1, false>(v, t, sm, tw, ofs, os);
-    sync();
-    fft_load_regs<M>(v, t, sm);
-    sync();
-    if constexpr (a == 1) {
-      fft_stage_rowoff<M, 16, b, true>(v, t, sm, tw, ofs, os);
-    } else {
-      fft_stage_rowoff<M, 16, b, false>(v, t, sm, tw, ofs, os);
-      sync();
-      fft_load_regs<M>(v, t, sm);
-      sync();
-      if constexpr (a == 2) {
-        fft_stage_rowoff<M, 16, b * 16, true>(v, t, sm, tw, ofs, os);
-      } else {
-        fft_stage_rowoff<M, 16, b * 16, false>(v, t, sm, tw, ofs, os);
-        sync();
-        fft_load_regs<M>(v, t, sm);
-        sync();
-        fft_stage_rowoff<M, 16, b * 256, true>(v, t, sm, tw, ofs, os);
-      }
-    }
-  } else {
-    if constexpr (a == 1) {
-      fft_stage_rowoff<M, 16, 1, true>(v, t, sm, tw, ofs, os);
-    } else {
-      fft_stage_rowoff<M, 16, 1, false>(v, t, sm, tw, ofs, os);
-      sync();
-      fft_load_regs<M>(v, t, sm);
-      sync();
-      if constexpr (a == 2) {
-        fft_stage_rowoff<M, 16, 16, true>(v, t, sm, tw, ofs, os);
-      } else {
-        fft_stage_rowoff<M, 16, 16, false>(v, t, sm, tw, ofs, os);
-        sync();
-        fft_load_regs<M>(v, t, sm);
-        sync();
-        fft_stage_rowoff<M, 16, 256, true>(v, t, sm, tw, ofs, os);
-      }
-    }
-  }
-}
-
 // Inverse (unnormalised) via conj(FFT(conj(x))).
 template <int M, class Sync = CtaSync>
 __device__ __forceinline__ void fft_inv(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,

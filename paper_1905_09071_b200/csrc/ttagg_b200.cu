@@ -60,7 +60,6 @@ constexpr int LLO = 1 << LSPLIT;
 // residue row blocks are padded to multiples of RB rows (8 x 16 B: every n2 row of the
 // exchange starts on a 128-byte line, so pass B's 8-row warp loads are whole lines)
 constexpr int RB = TTAGG_RB;
-constexpr int OFS_N = 22;  // per-row constants of fft_fwd_rowoff (16 first-stage + 3 x 2 inner)
 
 thread_local std::string g_err;
 
@@ -248,37 +247,23 @@ struct PMOut {
   cplx cn2;     // W_L^(n2 K) = W_N2^(n2)
 };
 
-#ifndef TTAGG_TW_IN_B
-#define TTAGG_TW_IN_B 0
-#endif
-#ifndef TTAGG_EX_CS
-#define TTAGG_EX_CS 1
-#endif
-#if TTAGG_EX_CS
-#define EXST stg_cs
-#else
-#define EXST sts_c
-#endif
 #ifndef TTAGG_B_JOINT
 #define TTAGG_B_JOINT 1
 #endif
-// With TTAGG_TW_IN_B the four-step twiddle W_L^(n2 kappa) is left to pass B
-// (both planes of row kappa take the same factor there), and pass A stores the
-// raw column outputs: P[kappa] = Zcol[kappa], M[K - kappa] = conj(Zcol[kappa]).
 __device__ __forceinline__ void emit_pm(const PassAArgs& a, const PMOut& o, int N1, int d, int j, int k1, cplx Y,
                                         cplx w) {
   if (a.dbg & 1) return;
-  const cplx Yw = TTAGG_TW_IN_B ? Y : cmul(Y, w);
-  const cplx Mv = TTAGG_TW_IN_B ? cconj(Y) : cmul(cconj(Yw), o.cn2);
-  if (k1 < a.res_cnt[j]) EXST(o.TP + a.res_base[j] + k1, Yw);
+  const cplx Yw = cmul(Y, w);
+  const cplx Mv = cmul(cconj(Yw), o.cn2);
+  if (k1 < a.res_cnt[j]) sts_c(o.TP + a.res_base[j] + k1, Yw);
   if (j == 0) {
     if (k1 == 0) {
-      EXST(o.TM + a.res_base[0], cconj(Y));
+      sts_c(o.TM + a.res_base[0], cconj(Y));
     } else if (2 * k1 >= N1) {
-      EXST(o.TM + a.res_base[0] + (N1 - k1), Mv);
+      sts_c(o.TM + a.res_base[0] + (N1 - k1), Mv);
     }
   } else if (2 * k1 >= N1) {
-    EXST(o.TM + a.res_base[d - j] + (N1 - 1 - k1), Mv);
+    sts_c(o.TM + a.res_base[d - j] + (N1 - 1 - k1), Mv);
   }
 }
 
@@ -459,11 +444,9 @@ struct PassBArgs {
   const double2* tabLhi;
   const int* rowkappa;
   double2* scratch;
-  double2* Sio;  // partial CP rank sums between pass-B chunks, [row block][E][128]
   long long L;
   int d, K, K_rows, C, kind, Rmax;
   int p0, p1;        // column pairs of this launch
-  int first, last;   // chunk flags: start the rank sum at zero / finish the rows
   int nrb;           // row blocks (CTAs loop over them)
   int ranks[MAXD + 1];
 };
@@ -499,7 +482,6 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
   double2* stP = smem;
   double2* stM = smem + STG;
   double2* Sb = smem + 2 * STG;  // CP rank sum, [k2][row] (conflict-free across the rows of a warp)
-  double2* Ost = Sb + ROWS * N2;  // [k][row]: offset constants of fft_fwd_rowoff (four-step twiddle)
   const size_t plane = (size_t)a.K_rows * N2;
   const int d = a.d;
   const int C = a.C;
@@ -525,40 +507,13 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
       S[i] = mk(0.0, 0.0);
       acc[i] = mk(0.0, 0.0);
     }
-    double2* Sio = a.Sio ? a.Sio + (size_t)rb * E * 128 + tid : nullptr;
     if constexpr (!TT) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) Sb[(t + T * i) * ROWS + rloc] = a.first ? make_double2(0.0, 0.0) : Sio[i * 128];
+      for (int i = 0; i < E; ++i) Sb[(t + T * i) * ROWS + rloc] = make_double2(0.0, 0.0);
     }
     // TT: fiber c -> (core lam, rn, rp), tracked incrementally
     int lam = 0, rn = 0, rp = 0;
-#if TTAGG_TW_IN_B
-    // the four-step twiddle W_L^(n2 kappa) of this row = a frequency offset of
-    // kappa/K in the row transforms: per-row stage constants (L = K N2)
-    {
-      const long long kap0 = valid ? max(a.rowkappa[rho], 0) : 0;
-      constexpr int b = fft_first_radix(N2) > 1 ? fft_first_radix(N2) : 16;
-      for (int k = t; k < OFS_N; k += T) {
-        long long ex = 0;
-        if (k < 16) {
-          if (k < b) ex = kap0 * k * (N2 / b);
-        } else {
-          const int s2 = (k - 16) >> 1, NS = b << (4 * s2);
-          ex = 16 * NS <= N2 ? ((k & 1) ? 4 : 1) * kap0 * (N2 / (16 * NS)) : 0;
-        }
-        const cplx w = twL(a.tabLlo, a.tabLhi, ex % a.L);
-        Ost[k * ROWS + rloc] = make_double2(w.x, w.y);
-      }
-    }
-#endif
-
-    auto row_fft = [&](cplx (&v)[E], double2* stage) {
-#if TTAGG_TW_IN_B
-      fft_fwd_rowoff<N2>(v, t, stage + rloc * SE, a.tw, Ost + rloc, ROWS);
-#else
-      fft_fwd<N2>(v, t, stage + rloc * SE, a.tw);
-#endif
-    };
+    auto row_fft = [&](cplx (&v)[E], double2* stage) { fft_fwd<N2>(v, t, stage + rloc * SE, a.tw); };
 
     auto process = [&](cplx (&X)[E], int c) {
       if constexpr (!TT) {
@@ -616,7 +571,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
       const bool more = p + 1 < a.p1;
       cplx vp[E], vm[E];
 #if TTAGG_B_JOINT
-      if constexpr (N2 == 256 && !TTAGG_TW_IN_B) {
+      if constexpr (N2 == 256) {
         cp_async_wait<0>();
 #pragma unroll
         for (int i = 0; i < E; ++i) {
@@ -660,11 +615,6 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     cp_async_wait<0>();
     __syncthreads();
     if constexpr (!TT) {
-      if (!a.last) {  // hand the partial rank sum to the next chunk
-#pragma unroll
-        for (int i = 0; i < E; ++i) Sio[i * 128] = Sb[(t + T * i) * ROWS + rloc];
-        continue;
-      }
 #pragma unroll
       for (int i = 0; i < E; ++i) S[i] = lds_c(Sb + (t + T * i) * ROWS + rloc);
     }
@@ -1208,7 +1158,7 @@ size_t smemB() {
   constexpr int T = fft_t(N2);
   constexpr int ROWS = 128 / T;
   constexpr size_t STG = std::max((size_t)ROWS * fft_smem_elems(N2), (size_t)fft_e(N2) * 128);
-  return (2 * STG + (size_t)ROWS * N2 + (size_t)ROWS * OFS_N) * sizeof(double2);
+  return (2 * STG + (size_t)ROWS * N2) * sizeof(double2);
 }
 
 template <int N2, bool TT>
@@ -1388,8 +1338,6 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
   b.nrb = (P->K_rows + rows - 1) / rows;
   b.p0 = 0;
   b.p1 = k->C_pad / 2;
-  b.first = b.last = 1;
-  b.Sio = nullptr;
   int gridB = b.nrb;
   if (k->kind == TTAGG_KIND_TT) {
     // The chain state (2 Rmax spectra per frequency) lives in a per-CTA global
