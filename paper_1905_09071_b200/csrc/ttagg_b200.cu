@@ -178,7 +178,8 @@ struct ttagg_kernel {
   int64_t N = 0;
   Geom g;
   int C = 0, C_pad = 0;
-  double* X = nullptr;  // [C_pad][Np]
+  double* X = nullptr;   // column pairs interleaved: pair p, element e -> double2 at X[(p Np + e) 2]
+  double* Xt = nullptr;  // tail columns (the loss's last factor), one per row: [ntail][Np]
   int R = 0;            // CP: local ranks
   int ranks[MAXD + 1] = {0};
   int core_off[MAXD + 1] = {0};
@@ -285,12 +286,12 @@ __global__ void __launch_bounds__(256) passA_kernel(const PassAArgs a) {
   const double2* zc = zbuf + g * N1;
   {
     const size_t e0 = (size_t)blockIdx.x * G * N1;
-    const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
-    const double* xb = xa + Np;
+    const double2* xp = reinterpret_cast<const double2*>(a.X) + (size_t)pair * Np + e0;
     double sa = 0.0, sb = 0.0;
     for (int i = tid; i < G * N1; i += blockDim.x) {
       const double w = state_at(a.nv, a.kv, a.alpha, e0 + i);
-      const double va = __ldg(xa + i) * w, vb = __ldg(xb + i) * w;
+      const double2 x = __ldg(xp + i);
+      const double va = x.x * w, vb = x.y * w;
       zbuf[i] = make_double2(va, vb);
       sa += va;
       sb += vb;
@@ -359,8 +360,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_big_kernel(const PassAArgs
   const int pair = a.pair0 + item / N2, n2 = item % N2;
   const size_t Np = (size_t)N1 * N2;
   const size_t e0 = (size_t)n2 * N1;
-  const double* xa = a.X + (size_t)(2 * pair) * Np + e0;
-  const double* xb = xa + Np;
+  const double2* xp = reinterpret_cast<const double2*>(a.X) + (size_t)pair * Np + e0;
   const double* nv = a.nv + e0;
   const double* kv = a.kv ? a.kv + e0 : nullptr;
   double2* exch = smem;
@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_big_kernel(const PassAArgs
       const int n1 = t + T * r;
       double w = __ldg(nv + n1);
       if (kv) w = __dadd_rn(w, __dmul_rn(a.alpha, __ldg(kv + n1)));
-      z[r] = mk(__ldg(xa + n1) * w, __ldg(xb + n1) * w);
+      const double2 x = __ldg(xp + n1);
+      z[r] = mk(x.x * w, x.y * w);
     }
   };
   {
@@ -1013,19 +1014,23 @@ __global__ void permute_kernel(const double* __restrict__ in, double* __restrict
   }
 }
 
-// scatter an N x R row-major factor (or a TT core slice) into perm-layout columns
-// column of (rank index j) goes to X[colmap[j]]; src element (o, j) at src[o*ld + j*jstride + off]
+// scatter an N x R row-major factor (or a TT core slice) into perm-layout columns:
+// column (rank index j) goes to column colmap[j] of X — pair-interleaved
+// (`paired`, the pass-A operand: column c at X[((c/2) Np + e) 2 + c%2]) or one
+// column per row (the combine's tail copy); src element (o, j) at src[o*ld + srcidx[j]]
 __global__ void scatter_columns_kernel(const double* __restrict__ src, long long N, int ld, int ncols,
                                        const int* __restrict__ srcidx, const int* __restrict__ colmap, double* X,
-                                       int N1, int N2) {
+                                       int N1, int N2, int paired) {
   const size_t Np = (size_t)N1 * N2;
   const int j = blockIdx.y;
   const int sj = srcidx[j];
-  double* dst = X + (size_t)colmap[j] * Np;
+  const int c = colmap[j];
+  double* dst = paired ? X + (size_t)(c >> 1) * 2 * Np + (c & 1) : X + (size_t)c * Np;
+  const int stride = paired ? 2 : 1;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < Np; e += (size_t)gridDim.x * blockDim.x) {
     const int n1 = (int)(e % N1), n2 = (int)(e / N1);
     const long long o = (long long)n1 * N2 + n2;
-    dst[e] = o < N ? src[o * ld + sj] : 0.0;
+    dst[e * stride] = o < N ? src[o * ld + sj] : 0.0;
   }
 }
 
@@ -1451,7 +1456,7 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
     const ttagg_kernel* k = ks[i];
     CombineOrder& o = A->o[i];
     o.p = pslot(i);
-    o.X = k->X;
+    o.X = k->Xt;
     o.tail = k->tail_cols;
     o.coef = wantQ ? k->coef : nullptr;
     o.ntail = k->ntail;
@@ -1610,6 +1615,7 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
     }
   }
   CUDA_TRY(cudaMemset(k->X, 0, std::max<size_t>(2, k->C_pad) * colbytes));
+  CUDA_TRY(cudaMalloc(&k->Xt, std::max<size_t>(1, k->R) * colbytes));
   std::vector<int> tails;
   if (k->R > 0) {
     double* dsrc = nullptr;
@@ -1625,14 +1631,21 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
       for (size_t j = 0; j < sel.size(); ++j) map[j] = (int)j * d + m;  // rank-major column order
       CUDA_TRY(cudaMemcpy(dmap, map.data(), map.size() * sizeof(int), cudaMemcpyHostToDevice));
       dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)sel.size());
-      scatter_columns_kernel<<<grid, 256>>>(dsrc, n_classes, (int)rank, (int)sel.size(), dsel, dmap, k->X, g.N1, g.N2);
+      scatter_columns_kernel<<<grid, 256>>>(dsrc, n_classes, (int)rank, (int)sel.size(), dsel, dmap, k->X, g.N1, g.N2, 1);
       CUDA_TRY(cudaGetLastError());
+      if (m == d - 1) {  // the loss's tail factor, one column per rank term
+        for (size_t j = 0; j < sel.size(); ++j) map[j] = (int)j;
+        CUDA_TRY(cudaMemcpy(dmap, map.data(), map.size() * sizeof(int), cudaMemcpyHostToDevice));
+        scatter_columns_kernel<<<grid, 256>>>(dsrc, n_classes, (int)rank, (int)sel.size(), dsel, dmap, k->Xt, g.N1,
+                                              g.N2, 0);
+        CUDA_TRY(cudaGetLastError());
+      }
     }
     CUDA_TRY(cudaDeviceSynchronize());
     cudaFree(dsrc);
     cudaFree(dsel);
     cudaFree(dmap);
-    for (int j = 0; j < k->R; ++j) tails.push_back(j * d + d - 1);
+    for (int j = 0; j < k->R; ++j) tails.push_back(j);  // rows of Xt
   }
   TRY(finish_upload(ctx, k, tails));
   *out = k;
@@ -1678,6 +1691,7 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   const size_t colbytes = (size_t)g.Np * sizeof(double);
   CUDA_TRY(cudaMalloc(&k->X, std::max<size_t>(2, k->C_pad) * colbytes));
   CUDA_TRY(cudaMemset(k->X, 0, std::max<size_t>(2, k->C_pad) * colbytes));
+  CUDA_TRY(cudaMalloc(&k->Xt, std::max<size_t>(1, k->ranks[d - 1]) * colbytes));
   double* dsrc = nullptr;
   int *dsel = nullptr, *dmap = nullptr;
   size_t maxcore = 0;
@@ -1700,8 +1714,15 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
       CUDA_TRY(cudaMemcpy(dmap, map.data(), rn_n * sizeof(int), cudaMemcpyHostToDevice));
       dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)rn_n);
       scatter_columns_kernel<<<grid, 256>>>(dsrc + (size_t)rp * n_classes * rn_n, n_classes, rn_n, rn_n, dsel, dmap,
-                                            k->X, g.N1, g.N2);
+                                            k->X, g.N1, g.N2, 1);
       CUDA_TRY(cudaGetLastError());
+      if (l == d - 1) {  // last core (rn_n = 1): the loss's tail fibers, one row of Xt per rp
+        const int row = rp;
+        CUDA_TRY(cudaMemcpy(dmap, &row, sizeof(int), cudaMemcpyHostToDevice));
+        scatter_columns_kernel<<<grid, 256>>>(dsrc + (size_t)rp * n_classes * rn_n, n_classes, rn_n, rn_n, dsel, dmap,
+                                              k->Xt, g.N1, g.N2, 0);
+        CUDA_TRY(cudaGetLastError());
+      }
       CUDA_TRY(cudaDeviceSynchronize());
     }
   }
@@ -1709,7 +1730,7 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   cudaFree(dsel);
   cudaFree(dmap);
   std::vector<int> tails;
-  for (int rp = 0; rp < k->ranks[d - 1]; ++rp) tails.push_back(k->core_off[d - 1] + rp);
+  for (int rp = 0; rp < k->ranks[d - 1]; ++rp) tails.push_back(rp);  // rows of Xt
   TRY(finish_upload(ctx, k, tails));
   *out = k;
   return TTAGG_OK;
@@ -1720,6 +1741,7 @@ int ttagg_kernel_free(ttagg_kernel* k) {
   cudaSetDevice(k->ctx->device);
   cudaDeviceSynchronize();
   cudaFree(k->X);
+  cudaFree(k->Xt);
   cudaFree(k->tail_cols);
   cudaFree(k->dots);
   cudaFree(k->coef);
