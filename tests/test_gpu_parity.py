@@ -285,3 +285,54 @@ def test_error_behaviour():
     with pytest.raises(_lib.TTaggError, match="exceeds"):
         g.rhs_cp_P(g.CPKernel((np.ones(((1 << 20) + 1, 1)), np.ones(((1 << 20) + 1, 1)))),
                    st(np.ones((1 << 20) + 1)))
+
+
+@pytest.mark.gpu
+def test_tt_rank_shards_sum_to_full_rhs():
+    """TT sharding over the first internal rank (construct.tt_rank_shard): the
+    partial RHS of every slice, each its own upload, sum to the unsharded RHS."""
+    import torch
+
+    from paper_1905_09071_b200.construct import tt_rank_shard
+
+    N = 5000
+    rng = np.random.default_rng(21)
+    cores = (rng.random((1, N, 6)), rng.random((6, N, 5)) / 6, rng.random((5, N, 1)))
+    n = rng.random(N) * np.exp(-np.arange(N) / 700.0)
+    full = g.rhs_total(g.KernelSet({3: g.TTKernel(cores)}), st(n)).s
+    ctx = _lib.get_context()
+    Np, _, _ = _lib.geometry(N)
+    dev = torch.device("cuda", ctx.device)
+    nt = torch.from_numpy(n).to(dev)
+    nperm = torch.zeros(Np, dtype=torch.float64, device=dev)
+    ctx.permute(N, nt.data_ptr(), nperm.data_ptr(), 0, None)
+    for world in (2, 3, 8):
+        acc = torch.zeros(Np, dtype=torch.float64, device=dev)
+        for r in range(world):
+            sl = tt_rank_shard(cores, world, r)
+            if sl is None:
+                continue
+            part = torch.zeros(Np, dtype=torch.float64, device=dev)
+            ctx.rhs_perm([ctx.upload_tt(sl)], nperm.data_ptr(), None, 0.0, part.data_ptr(), None)
+            acc += part
+        out = torch.empty(N, dtype=torch.float64, device=dev)
+        ctx.permute(N, acc.data_ptr(), out.data_ptr(), 1, None)
+        torch.cuda.synchronize()
+        assert rel_inf(out.cpu().numpy(), full) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_c4_cross_kernel_vs_oracle():
+    """Config C4's kernel set built by construct.c4_kernels (TT-cross d = 3,
+    exact d = 2) at N = 4096: GPU RHS against the oracle on the same cores."""
+    from paper_1905_09071_b200.construct import c4_kernels
+
+    N = 4096
+    (c1, c2), cores3 = c4_kernels(N, rank=16)
+    n = np.exp(-np.arange(1, N + 1) / 256.0)
+    ks = g.KernelSet({2: g.TTKernel((c1, c2)), 3: g.TTKernel(cores3)})
+    res = g.rhs_total(ks, st(n))
+    ref = orc.rhs_total({2: {"kind": "tt", "arrays": (c1, c2)}, 3: {"kind": "tt", "arrays": cores3}}, n)
+    assert rel_inf(res.p, ref[0]) <= TOL
+    assert rel_inf(res.q, ref[1]) <= TOL
+    assert rel_inf(res.s, ref[2]) <= TOL
