@@ -516,7 +516,10 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     int lam = 0, rn = 0, rp = 0;
     auto row_fft = [&](cplx (&v)[E], double2* stage) { fft_fwd<N2>(v, t, stage + rloc * SE, a.tw); };
 
-    auto process = [&](cplx (&X)[E], int c) {
+    // TT: the chain state of the pair's first column is prefetched into the
+    // (otherwise unused) rank-sum region Sb with cp.async before the row FFTs
+    bool pre = false;
+    auto process = [&](cplx (&X)[E], int c, bool from_sb) {
       if constexpr (!TT) {
         const int m = c % d;  // rank-major columns: c = r d + m
         if (m == 0) {
@@ -544,7 +547,8 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
             for (int i = 0; i < E; ++i) acc[i] = mk(0.0, 0.0);
           }
 #pragma unroll
-          for (int i = 0; i < E; ++i) acc[i] = cadd(acc[i], cmul(lds_c(st((lam - 1) & 1, rp, i)), X[i]));
+          for (int i = 0; i < E; ++i)
+            acc[i] = cadd(acc[i], cmul(from_sb ? lds_c(Sb + i * 128 + tid) : lds_c(st((lam - 1) & 1, rp, i)), X[i]));
           if (rp == rp_n - 1) {
             if (lam == d - 1) {
 #pragma unroll
@@ -579,6 +583,15 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
           vp[i] = lds_c(stP + i * 128 + tid);
           vm[i] = lds_c(stM + i * 128 + tid);
         }
+        if constexpr (TT) {
+          pre = lam >= 1;
+          if (pre) {  // state of column 2p: written (if at all) by earlier columns of this thread
+            __threadfence_block();
+#pragma unroll
+            for (int i = 0; i < E; ++i) cp_async16(Sb + i * 128 + tid, st((lam - 1) & 1, rp, i), true);
+          }
+          cp_async_commit();
+        }
         __syncthreads();
         fft_fwd2<N2>(vp, vm, t, stP + rloc * SE, stM + rloc * SE, a.tw);
         if (more) {
@@ -588,6 +601,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
           cp_async_commit();
           cp_async_commit();
         }
+        if constexpr (TT) cp_async_wait<2>();  // the state group (P/M of p+1 may fly on)
       } else
 #endif
       {
@@ -610,8 +624,9 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
         vp[i] = cscale(cadd(P, vm[i]), 0.5);
         vm[i] = cscale(mul_mi(csub(P, vm[i])), 0.5);
       }
-      process(vp, 2 * p);
-      if (2 * p + 1 < C) process(vm, 2 * p + 1);
+      process(vp, 2 * p, pre);
+      if (2 * p + 1 < C) process(vm, 2 * p + 1, false);
+      pre = false;
     }
     cp_async_wait<0>();
     __syncthreads();
