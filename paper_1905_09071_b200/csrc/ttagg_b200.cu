@@ -232,7 +232,6 @@ struct PassAArgs {
   int d, N2, K_rows, nblk, want_T;
   int pair0;  // first column pair of this launch (pass-A chunk)
   int res_base[MAXRES], res_cnt[MAXRES];
-  int dbg;  // debug: 1 skip stores, 2 skip FFTs, 4 skip input loads
 };
 
 // Emit one column-transform output of the packed pair z = a + i b
@@ -253,7 +252,6 @@ struct PMOut {
 #endif
 __device__ __forceinline__ void emit_pm(const PassAArgs& a, const PMOut& o, int N1, int d, int j, int k1, cplx Y,
                                         cplx w) {
-  if (a.dbg & 1) return;
   const cplx Yw = cmul(Y, w);
   const cplx Mv = cmul(cconj(Yw), o.cn2);
   if (k1 < a.res_cnt[j]) sts_c(o.TP + a.res_base[j] + k1, Yw);
@@ -333,10 +331,6 @@ __global__ void __launch_bounds__(256) passA_kernel(const PassAArgs a) {
   }
 }
 
-// ---- L2 prefetch (bulk-async engine)
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // Pass A for column transforms of >= 32 threads (N1 >= 512): one CTA (one
 // thread group, T threads) = one work item (column pair, n2), 70 KB of shared
@@ -1297,14 +1291,6 @@ int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
   a.nblk = k->nblk;
   a.want_T = wantP ? 1 : 0;
   a.pair0 = 0;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("TTAGG_DEBUG_PASSA");
-      dbg = e ? atoi(e) : 0;
-    }
-    a.dbg = dbg;
-  }
   for (int j = 0; j < MAXRES; ++j) {
     a.res_base[j] = P->res_base[j];
     a.res_cnt[j] = P->res_cnt[j];
