@@ -95,16 +95,30 @@ def test_c5_literal_failure_and_normalised_trajectory(golden):
     assert_rows(series.rows(), c["norm4096_rows"], TRAJ_TOL)
 
 
-def test_fused_integrate_matches_stepwise_and_rk2_step():
-    """The device-resident fused loop (ttagg_rk2) == host-orchestrated rk2_step."""
+def test_fused_integrate_matches_stepwise_and_rk2_step(monkeypatch):
+    """The device-resident fused loop (ttagg_rk2), its per-record-interval form
+    (on_record) and the host-orchestrated rk2_step loop (taken when the
+    rhs_total seam is replaced) agree."""
+    import paper_1905_09071_b200.integrator as integrator_mod
+
     cfg = CONFIGS["C5"]
     N = 1 << 13
     ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors(N).items()})
     n0 = initial_state("c5", N, normalised=True)
     fused_final, fused = g.integrate(Cfg(n0, cfg.dt, 7, 2), kernels=ks)
-    seen = []
-    step_final, stepped = g.integrate(Cfg(n0, cfg.dt, 7, 2), kernels=ks, on_record=lambda s, x: seen.append(s))
+    seen, states = [], []
+    chunk_final, chunked = g.integrate(Cfg(n0, cfg.dt, 7, 2), kernels=ks,
+                                       on_record=lambda s, x: (seen.append(s), states.append(x.n.copy())))
     assert seen == [0, 2, 4, 6]
+    assert rel_inf(fused_final.n, chunk_final.n) <= 1e-13
+    assert_rows(fused.rows(), chunked.rows(), 1e-13)
+    orig = integrator_mod.rhs_total
+    monkeypatch.setattr(integrator_mod, "rhs_total", lambda *a, **k: orig(*a, **k))
+    seen2 = []
+    step_final, stepped = g.integrate(Cfg(n0, cfg.dt, 7, 2), kernels=ks, on_record=lambda s, x: seen2.append(x.n.copy()))
+    assert len(seen2) == 4
+    for a, b in zip(states, seen2):
+        assert rel_inf(a, b) <= 1e-13
     assert rel_inf(fused_final.n, step_final.n) <= 1e-13
     assert_rows(fused.rows(), stepped.rows(), 1e-12)
     s = g.ConcentrationState(n0)
