@@ -1057,7 +1057,13 @@ int ensure(void** p, size_t* have, size_t need, bool zero = false) {
     cudaGetLastError();
     return fail(TTAGG_ERR_NOMEM, "device allocation of " + std::to_string(alloc) + " bytes failed: " + cudaGetErrorString(e));
   }
-  if (zero) CUDA_TRY(cudaMemset(*p, 0, alloc));
+  if (zero) {
+    // cudaMemset runs on the legacy default stream, which the context's
+    // non-blocking streams do not wait for: complete it before any kernel can
+    // touch the buffer
+    CUDA_TRY(cudaMemset(*p, 0, alloc));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
   *have = alloc;
   return TTAGG_OK;
 }
@@ -1429,7 +1435,12 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
   std::stable_sort(order.begin(), order.end(),
                    [&](int x, int y) { return order_cost(ks[x]) > order_cost(ks[y]); });
   auto pslot = [&](int i) { return wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr; };
-  const bool conc = wantP && nk > 1;
+  static int serial = -1;  // TTAGG_SERIAL=1: one stream (diagnostics)
+  if (serial < 0) {
+    const char* e = getenv("TTAGG_SERIAL");
+    serial = e ? atoi(e) : 0;
+  }
+  const bool conc = wantP && nk > 1 && !serial;
   if (!conc) {
     for (int i : order) {
       TRY(run_passA(ctx, ks[i], nv, kv, alpha, wantP, wantQ, ctx->work[i], st));

@@ -336,3 +336,23 @@ def test_c4_cross_kernel_vs_oracle():
     assert rel_inf(res.p, ref[0]) <= TOL
     assert rel_inf(res.q, ref[1]) <= TOL
     assert rel_inf(res.s, ref[2]) <= TOL
+
+
+@pytest.mark.gpu
+def test_workspace_regrowth_between_kernel_sets():
+    """A kernel set with fewer column pairs sizes the per-order workspaces
+    first; the next (larger) set must regrow and re-zero them before any of
+    its passes run on the context's streams (regression: the zeroing once
+    raced the first pass A on a non-blocking stream)."""
+    cfg = CONFIGS["C5"]
+    N = 1 << 16
+    rng = np.random.default_rng(5)
+    n = initial_state("c5", N)
+    small = g.KernelSet({d: g.TTKernel(tuple(rng.random((r0, N, r1)) for r0, r1 in zip((1,) + (2,) * (d - 1), (2,) * (d - 1) + (1,))))
+                         for d in cfg.orders})
+    big = g.KernelSet({d: g.CPKernel(permutation_power_cp(cfg.exponents[:d], N)) for d in cfg.orders})
+    g.rhs_total(small, st(n))
+    got = g.rhs_total(big, st(n))
+    ref = orc.rhs_total({d: {"kind": "cp", "arrays": big[d].factors} for d in big.orders}, n)
+    assert rel_inf(got.p, ref[0]) <= TOL
+    assert rel_inf(got.s, ref[2]) <= TOL
