@@ -187,6 +187,9 @@ struct ttagg_kernel {
   int ntail = 0;
   int* tail_cols = nullptr;
   int nblk = 0;  // pass-A blocks per column (dot partials)
+  int* fdesc = nullptr;  // TT: descriptors of the uploaded (live) fibers
+  int* cidx = nullptr;   // TT: full fiber index -> uploaded column or -1
+  int C_full = 0;        // TT: fibers before dropping
   double* dots = nullptr;
   double* coef = nullptr;
   OrderPlan* plan = nullptr;
@@ -444,7 +447,20 @@ struct PassBArgs {
   int p0, p1;        // column pairs of this launch
   int nrb;           // row blocks (CTAs loop over them)
   int ranks[MAXD + 1];
+  const int* fdesc;  // TT: per uploaded fiber, packed (core, rn, rp, first, last, noop)
 };
+
+// TT fiber descriptor: the uploaded columns are the live fibers only (all-zero
+// fibers and fibers on a chain path that is zero are dropped at upload), in
+// core-major, rn-major, rp-inner order; first/last mark the first and last
+// live fiber that feeds chain state (core, rn).
+constexpr int FD_FIRST = 1 << 20, FD_LAST = 1 << 21, FD_NOOP = 1 << 22;
+__host__ __device__ constexpr int fd_pack(int lam, int rn, int rp, bool first, bool last) {
+  return lam | (rn << 4) | (rp << 12) | (first ? FD_FIRST : 0) | (last ? FD_LAST : 0);
+}
+__device__ __forceinline__ int fd_lam(int f) { return f & 15; }
+__device__ __forceinline__ int fd_rn(int f) { return (f >> 4) & 255; }
+__device__ __forceinline__ int fd_rp(int f) { return (f >> 12) & 255; }
 
 // ---- per-thread asynchronous 16-byte copies (global -> shared), zero-fill when !ok
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
@@ -506,8 +522,6 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
 #pragma unroll
       for (int i = 0; i < E; ++i) Sb[(t + T * i) * ROWS + rloc] = make_double2(0.0, 0.0);
     }
-    // TT: fiber c -> (core lam, rn, rp), tracked incrementally
-    int lam = 0, rn = 0, rp = 0;
     auto row_fft = [&](cplx (&v)[E], double2* stage) { fft_fwd<N2>(v, t, stage + rloc * SE, a.tw); };
 
     // TT: the chain state of the pair's first column is prefetched into the
@@ -531,19 +545,21 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
           }
         }
       } else {
-        const int rp_n = a.ranks[lam];
+        const int f = __ldg(a.fdesc + c);
+        if (f & FD_NOOP) return;
+        const int lam = fd_lam(f), rn = fd_rn(f), rp = fd_rp(f);
         if (lam == 0) {
 #pragma unroll
           for (int i = 0; i < E; ++i) sts_c(st(0, rn, i), X[i]);
         } else {
-          if (rp == 0) {
+          if (f & FD_FIRST) {
 #pragma unroll
             for (int i = 0; i < E; ++i) acc[i] = mk(0.0, 0.0);
           }
 #pragma unroll
           for (int i = 0; i < E; ++i)
             acc[i] = cadd(acc[i], cmul(from_sb ? lds_c(Sb + i * 128 + tid) : lds_c(st((lam - 1) & 1, rp, i)), X[i]));
-          if (rp == rp_n - 1) {
+          if (f & FD_LAST) {
             if (lam == d - 1) {
 #pragma unroll
               for (int i = 0; i < E; ++i) S[i] = acc[i];
@@ -551,14 +567,6 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
 #pragma unroll
               for (int i = 0; i < E; ++i) sts_c(st(lam & 1, rn, i), acc[i]);
             }
-          }
-        }
-        // advance (lam, rn, rp) in fiber order: rn-major, rp inner
-        if (++rp == rp_n) {
-          rp = 0;
-          if (++rn == a.ranks[lam + 1]) {
-            rn = 0;
-            ++lam;
           }
         }
       }
@@ -578,11 +586,12 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
           vm[i] = lds_c(stM + i * 128 + tid);
         }
         if constexpr (TT) {
-          pre = lam >= 1;
+          const int f = __ldg(a.fdesc + 2 * p);
+          pre = !(f & FD_NOOP) && fd_lam(f) >= 1;
           if (pre) {  // state of column 2p: written (if at all) by earlier columns of this thread
             __threadfence_block();
 #pragma unroll
-            for (int i = 0; i < E; ++i) cp_async16(Sb + i * 128 + tid, st((lam - 1) & 1, rp, i), true);
+            for (int i = 0; i < E; ++i) cp_async16(Sb + i * 128 + tid, st((fd_lam(f) - 1) & 1, fd_rp(f), i), true);
           }
           cp_async_commit();
         }
@@ -614,9 +623,11 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
       }
 #pragma unroll
       for (int i = 0; i < E; ++i) {
+        // 2A = P + M, 2B = -i (P - M); the 2^d this leaves on every order-d
+        // product is removed exactly in pass C's scale
         const cplx P = vp[i];
-        vp[i] = cscale(cadd(P, vm[i]), 0.5);
-        vm[i] = cscale(mul_mi(csub(P, vm[i])), 0.5);
+        vp[i] = cadd(P, vm[i]);
+        vm[i] = mul_mi(csub(P, vm[i]));
       }
       process(vp, 2 * p, pre);
       if (2 * p + 1 < C) process(vm, 2 * p + 1, false);
@@ -710,6 +721,7 @@ struct QArgs {
   int nblk, C, kind, d, R;
   int ranks[MAXD + 1];
   int core_off[MAXD + 1];
+  const int* cidx;  // TT: full fiber index -> uploaded column, -1 if dropped (contributes 0)
 };
 
 __global__ void qcoef_kernel(const QArgs a) {
@@ -730,13 +742,17 @@ __global__ void qcoef_kernel(const QArgs a) {
     }
   } else if (threadIdx.x == 0) {
     // w = V1 V2 ... V_{d-1}, V_l[rp, rn] = sum_i H_l[rp, i, rn] n_i   (rhs.py:305-338)
+    auto V = [&](int full) {
+      const int c = a.cidx[full];
+      return c < 0 ? 0.0 : sdot[c];
+    };
     double w[64], wn[64];
-    for (int rn = 0; rn < a.ranks[1]; ++rn) w[rn] = sdot[a.core_off[0] + rn];
+    for (int rn = 0; rn < a.ranks[1]; ++rn) w[rn] = V(a.core_off[0] + rn);
     for (int lam = 1; lam < a.d - 1; ++lam) {
       const int rp_n = a.ranks[lam], rn_n = a.ranks[lam + 1];
       for (int rn = 0; rn < rn_n; ++rn) {
         double s = 0.0;
-        for (int rp = 0; rp < rp_n; ++rp) s += w[rp] * sdot[a.core_off[lam] + rn * rp_n + rp];
+        for (int rp = 0; rp < rp_n; ++rp) s += w[rp] * V(a.core_off[lam] + rn * rp_n + rp);
         wn[rn] = s;
       }
       for (int rn = 0; rn < rn_n; ++rn) w[rn] = wn[rn];
@@ -1319,6 +1335,7 @@ int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       q.ranks[i] = k->ranks[i];
       q.core_off[i] = k->core_off[i];
     }
+    q.cidx = k->cidx;
     ProfScope ps(ctx, 3, st, k->d);
     qcoef_kernel<<<1, 256, std::max(1, k->C_pad) * sizeof(double), st>>>(q);
     CUDA_TRY(cudaGetLastError());
@@ -1346,6 +1363,7 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
   b.kind = k->kind;
   b.Rmax = k->Rmax;
   for (int i = 0; i <= MAXD; ++i) b.ranks[i] = k->ranks[i];
+  b.fdesc = k->fdesc;
   const int rows = rowsB(g.N2);
   b.nrb = (P->K_rows + rows - 1) / rows;
   b.p0 = 0;
@@ -1377,7 +1395,7 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
   c.tw = ctx->tw4096;
   c.tabK = P->tabK;
   c.N = g.N;
-  c.invL = 1.0 / (double)P->L;
+  c.invL = std::ldexp(1.0 / (double)P->L, -k->d);  // 1/L and pass B's 2^-d
   double f = 1.0;
   for (int i = 2; i <= k->d; ++i) f *= i;
   c.fact = f;
@@ -1696,10 +1714,77 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
     C += k->ranks[l] * k->ranks[l + 1];
   }
   k->core_off[d] = C;
-  k->C = C;
-  k->C_pad = (C + 1) & ~1;
+  k->C_full = C;
+  for (int l = 0; l < d; ++l)
+    if (!cores[l]) {
+      delete k;
+      return fail(TTAGG_ERR_ARG, "null core");
+    }
+  // Live fibers.  A fiber H_l[rp, :, rn] that is identically zero adds nothing
+  // to the chain (rhs.py:277-290) nor to the loss contraction (rhs.py:305-338);
+  // neither does a fiber whose input state (l, rp) is fed only by dropped
+  // fibers, nor one whose output state (l+1, rn) feeds no live fiber.  The
+  // exactly-structured kernels of the reference (build_brownian_tt,
+  // kernels.py:332-363) are mostly such zeros.
+  auto fidx = [&](int l, int rp, int rn) { return k->core_off[l] + rn * k->ranks[l] + rp; };
+  std::vector<char> live(C, 0);
+  {
+    std::vector<std::vector<char>> fwd(d + 1), used(d + 1);
+    for (int l = 0; l <= d; ++l) {
+      fwd[l].assign(k->ranks[l], 0);
+      used[l].assign(k->ranks[l], 0);
+    }
+    fwd[0][0] = 1;
+    used[d][0] = 1;
+    std::vector<char> nz(C, 0);
+    for (int l = 0; l < d; ++l) {
+      const int rp_n = k->ranks[l], rn_n = k->ranks[l + 1];
+      const double* H = cores[l];
+      for (int rp = 0; rp < rp_n; ++rp)
+        for (int64_t o = 0; o < n_classes; ++o) {
+          const double* row = H + ((size_t)rp * n_classes + o) * rn_n;
+          for (int rn = 0; rn < rn_n; ++rn)
+            if (row[rn] != 0.0 || row[rn] != row[rn]) nz[fidx(l, rp, rn)] = 1;  // nonzero or NaN
+        }
+      for (int rn = 0; rn < rn_n; ++rn)
+        for (int rp = 0; rp < rp_n; ++rp)
+          if (nz[fidx(l, rp, rn)] && fwd[l][rp]) {
+            live[fidx(l, rp, rn)] = 1;
+            fwd[l + 1][rn] = 1;
+          }
+    }
+    for (int l = d - 1; l >= 0; --l)
+      for (int rn = 0; rn < k->ranks[l + 1]; ++rn)
+        for (int rp = 0; rp < k->ranks[l]; ++rp) {
+          char& f = live[fidx(l, rp, rn)];
+          f = f && used[l + 1][rn];
+          if (f) used[l][rp] = 1;
+        }
+  }
+  std::vector<int> cidx(C, -1), desc;
+  for (int l = 0; l < d; ++l)
+    for (int rn = 0; rn < k->ranks[l + 1]; ++rn) {
+      int first = -1, last = -1;
+      for (int rp = 0; rp < k->ranks[l]; ++rp)
+        if (live[fidx(l, rp, rn)]) {
+          if (first < 0) first = rp;
+          last = rp;
+        }
+      for (int rp = 0; rp < k->ranks[l]; ++rp)
+        if (live[fidx(l, rp, rn)]) {
+          cidx[fidx(l, rp, rn)] = (int)desc.size();
+          desc.push_back(fd_pack(l, rn, rp, rp == first, rp == last));
+        }
+    }
+  if (desc.empty()) desc.push_back(FD_NOOP);  // an all-zero kernel: one zero column
+  k->C = (int)desc.size();
+  k->C_pad = (k->C + 1) & ~1;
   k->Rmax = Rmax;
   k->R = k->ranks[d - 1];
+  CUDA_TRY(cudaMalloc(&k->fdesc, desc.size() * sizeof(int)));
+  CUDA_TRY(cudaMemcpy(k->fdesc, desc.data(), desc.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&k->cidx, (size_t)C * sizeof(int)));
+  CUDA_TRY(cudaMemcpy(k->cidx, cidx.data(), (size_t)C * sizeof(int), cudaMemcpyHostToDevice));
   const size_t colbytes = (size_t)g.Np * sizeof(double);
   CUDA_TRY(cudaMalloc(&k->X, std::max<size_t>(2, k->C_pad) * colbytes));
   CUDA_TRY(cudaMemset(k->X, 0, std::max<size_t>(2, k->C_pad) * colbytes));
@@ -1712,26 +1797,31 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   CUDA_TRY(cudaMalloc(&dsel, 64 * 64 * sizeof(int)));
   CUDA_TRY(cudaMalloc(&dmap, 64 * 64 * sizeof(int)));
   for (int l = 0; l < d; ++l) {
-    if (!cores[l]) return fail(TTAGG_ERR_ARG, "null core");
     const int rp_n = k->ranks[l], rn_n = k->ranks[l + 1];
     CUDA_TRY(cudaMemcpy(dsrc, cores[l], (size_t)rp_n * n_classes * rn_n * sizeof(double), cudaMemcpyHostToDevice));
     // element H[rp, o, rn] at rp*N*rn_n + o*rn_n + rn.  Handle one rp slab at a time:
     for (int rp = 0; rp < rp_n; ++rp) {
-      std::vector<int> sidx(rn_n), map(rn_n);
-      for (int rn = 0; rn < rn_n; ++rn) {
-        sidx[rn] = rn;
-        map[rn] = k->core_off[l] + rn * rp_n + rp;  // fiber order: rn-major, rp inner
+      std::vector<int> sidx, map;
+      for (int rn = 0; rn < rn_n; ++rn)
+        if (cidx[fidx(l, rp, rn)] >= 0) {
+          sidx.push_back(rn);
+          map.push_back(cidx[fidx(l, rp, rn)]);  // uploaded column of this live fiber
+        }
+      const int nsel = (int)sidx.size();
+      if (nsel > 0) {
+        CUDA_TRY(cudaMemcpy(dsel, sidx.data(), nsel * sizeof(int), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dmap, map.data(), nsel * sizeof(int), cudaMemcpyHostToDevice));
+        dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)nsel);
+        scatter_columns_kernel<<<grid, 256>>>(dsrc + (size_t)rp * n_classes * rn_n, n_classes, rn_n, nsel, dsel,
+                                              dmap, k->X, g.N1, g.N2, 1);
+        CUDA_TRY(cudaGetLastError());
       }
-      CUDA_TRY(cudaMemcpy(dsel, sidx.data(), rn_n * sizeof(int), cudaMemcpyHostToDevice));
-      CUDA_TRY(cudaMemcpy(dmap, map.data(), rn_n * sizeof(int), cudaMemcpyHostToDevice));
-      dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)rn_n);
-      scatter_columns_kernel<<<grid, 256>>>(dsrc + (size_t)rp * n_classes * rn_n, n_classes, rn_n, rn_n, dsel, dmap,
-                                            k->X, g.N1, g.N2, 1);
-      CUDA_TRY(cudaGetLastError());
       if (l == d - 1) {  // last core (rn_n = 1): the loss's tail fibers, one row of Xt per rp
-        const int row = rp;
+        const int zero = 0, row = rp;
+        CUDA_TRY(cudaMemcpy(dsel, &zero, sizeof(int), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(dmap, &row, sizeof(int), cudaMemcpyHostToDevice));
-        scatter_columns_kernel<<<grid, 256>>>(dsrc + (size_t)rp * n_classes * rn_n, n_classes, rn_n, rn_n, dsel, dmap,
+        dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), 1u);
+        scatter_columns_kernel<<<grid, 256>>>(dsrc + (size_t)rp * n_classes * rn_n, n_classes, rn_n, 1, dsel, dmap,
                                               k->Xt, g.N1, g.N2, 0);
         CUDA_TRY(cudaGetLastError());
       }
@@ -1757,6 +1847,8 @@ int ttagg_kernel_free(ttagg_kernel* k) {
   cudaFree(k->tail_cols);
   cudaFree(k->dots);
   cudaFree(k->coef);
+  cudaFree(k->fdesc);
+  cudaFree(k->cidx);
   delete k;
   return TTAGG_OK;
 }
