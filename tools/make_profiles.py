@@ -9,8 +9,8 @@
       profiles/<tag>_roofline_traffic.json (DRAM bytes per launch, keyed "passA d=5")
 
 Kernels are attributed to orders from their grid: pass A launches npairs*N2
-CTAs, pass B ceil(K_rows/8) with K_rows ~ d*N1/2; qcoef/pass C follow their
-order's pass A/B in issue order.
+CTAs, pass B ceil(K_rows/8) with K_rows ~ d*N1/2; pass C follows its order's
+pass B, qcoef its order's pass A (in pass-A issue order).
 """
 import csv
 import io
@@ -39,12 +39,15 @@ def grid_count(g):
 
 
 def label(rows):
-    """[(kernel, grid, value...)] in issue order -> labels 'passA d=5' etc."""
-    out, cur = [], None
+    """[(kernel, grid, value...)] in issue order -> labels 'passA d=5' etc.
+    qcoef launches (fill stream) belong to the oldest pass A whose qcoef has
+    not been seen yet; pass C follows its own order's pass B."""
+    out, cur, pending = [], None, []
     for name, grid in rows:
         k = short(name)
         if k.startswith("passA"):
             cur = C5_PAIRS.get(grid // N2)
+            pending.append(cur)
             out.append(f"passA d={cur}")
         elif k.startswith("passB"):
             cur = round(grid / (N1 // 16))
@@ -52,16 +55,9 @@ def label(rows):
         elif k.startswith("passC"):
             out.append(f"passC d={cur}")
         elif k.startswith("qcoef"):
-            out.append(f"qcoef d={cur}")
+            out.append(f"qcoef d={pending.pop(0) if pending else None}")
         else:
             out.append(k)
-    # a capture window that starts mid-RHS: the leading qcoef/pass C belong to
-    # the order whose own qcoef/pass C is missing from the window
-    for kind in ("qcoef", "passC"):
-        have = {o for o in out if o.startswith(kind) and not o.endswith("None")}
-        orders = sorted({o.split("=")[1] for o in out if o.startswith("passA")})
-        missing = [d for d in orders if f"{kind} d={d}" not in have]
-        out = [f"{kind} d={missing[0]}" if o == f"{kind} d=None" and len(missing) == 1 else o for o in out]
     return out
 
 
