@@ -512,12 +512,12 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
       for (int i = 0; i < E; ++i) cp_async16(stage + i * 128 + tid, src + (size_t)(t + T * i) * a.K_rows, valid);
       cp_async_commit();
     };
-    cplx S[E], acc[E];
+    // CP: running product over the modes of one rank term.  TT: chain
+    // accumulator of the current state (core, rn); the last group processed
+    // is the last core's, so after the loop it holds the chain result.
+    cplx acc[E];
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      S[i] = mk(0.0, 0.0);
-      acc[i] = mk(0.0, 0.0);
-    }
+    for (int i = 0; i < E; ++i) acc[i] = mk(0.0, 0.0);
     if constexpr (!TT) {
 #pragma unroll
       for (int i = 0; i < E; ++i) Sb[(t + T * i) * ROWS + rloc] = make_double2(0.0, 0.0);
@@ -559,14 +559,9 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
 #pragma unroll
           for (int i = 0; i < E; ++i)
             acc[i] = cadd(acc[i], cmul(from_sb ? lds_c(Sb + i * 128 + tid) : lds_c(st((lam - 1) & 1, rp, i)), X[i]));
-          if (f & FD_LAST) {
-            if (lam == d - 1) {
+          if ((f & FD_LAST) && lam < d - 1) {
 #pragma unroll
-              for (int i = 0; i < E; ++i) S[i] = acc[i];
-            } else {
-#pragma unroll
-              for (int i = 0; i < E; ++i) sts_c(st(lam & 1, rn, i), acc[i]);
-            }
+            for (int i = 0; i < E; ++i) sts_c(st(lam & 1, rn, i), acc[i]);
           }
         }
       }
@@ -635,10 +630,9 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();
-    if constexpr (!TT) {
+    cplx S[E];
 #pragma unroll
-      for (int i = 0; i < E; ++i) S[i] = lds_c(Sb + (t + T * i) * ROWS + rloc);
-    }
+    for (int i = 0; i < E; ++i) S[i] = TT ? acc[i] : lds_c(Sb + (t + T * i) * ROWS + rloc);
 
     // (d-1)-position shift (s'[t] = s[t-(d-1)] <=> S'[k] = S[k] W_L^{(d-1)k}), inverse row FFT, inverse twiddle, Hermitian weight
     const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
