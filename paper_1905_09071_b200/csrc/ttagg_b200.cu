@@ -718,13 +718,17 @@ struct QArgs {
   const int* cidx;  // TT: full fiber index -> uploaded column, -1 if dropped (contributes 0)
 };
 
-__global__ void qcoef_kernel(const QArgs a) {
+__global__ void __launch_bounds__(1024) qcoef_kernel(const QArgs a) {
   extern __shared__ double sdot[];
-  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+  // one warp per column: coalesced partial loads, fixed-order lane sums then
+  // a fixed shuffle tree (deterministic)
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x >> 5; c < a.C; c += nw) {
     double s = 0.0;
     const double* p = a.dots + (size_t)c * a.nblk;
-    for (int b = 0; b < a.nblk; ++b) s += p[b];
-    sdot[c] = s;
+    for (int b = lane; b < a.nblk; b += 32) s += p[b];
+    s = warp_sum(s);
+    if (lane == 0) sdot[c] = s;
   }
   __syncthreads();
   if (a.kind == TTAGG_KIND_CP) {
@@ -1150,6 +1154,7 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   if constexpr (T >= 32) {
     const size_t smem = (size_t)fft_smem_elems(N1) * sizeof(double2);
     TRY(set_smem(passA_big_kernel<N1>, smem));
+
     passA_big_kernel<N1><<<npairs * N2, T, smem, st>>>(a);
     CUDA_TRY(cudaGetLastError());
     return TTAGG_OK;
@@ -1331,7 +1336,9 @@ int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
     }
     q.cidx = k->cidx;
     ProfScope ps(ctx, 3, st, k->d);
-    qcoef_kernel<<<1, 256, std::max(1, k->C_pad) * sizeof(double), st>>>(q);
+    const size_t qsm = std::max(1, k->C_pad) * sizeof(double);
+    TRY(set_smem(qcoef_kernel, qsm));
+    qcoef_kernel<<<1, 1024, qsm, st>>>(q);
     CUDA_TRY(cudaGetLastError());
     ++ctx->launches;
   }
