@@ -46,6 +46,7 @@ extern "C" {
 
 #define TTAGG_KIND_CP 1
 #define TTAGG_KIND_TT 2
+#define TTAGG_KIND_DENSE 3
 
 typedef struct ttagg_ctx ttagg_ctx;       /* one per CUDA device (workspaces, tables) */
 typedef struct ttagg_kernel ttagg_kernel; /* one uploaded collision kernel of order d */
@@ -75,6 +76,14 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank,
  * (ranks[l], N, ranks[l+1]) row-major. */
 int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ranks,
                     const double* const* cores, ttagg_kernel** out);
+
+/* Upload a dense kernel (replaces DenseKernel, kernels.py:218-238, for the
+ * direct-summation operators rhs_dense_P / rhs_dense_Q, rhs.py:202-227).
+ * values: host pointer to N^d fp64 coefficients in row-major index order;
+ * N^d must not exceed 2^26 (DENSE_RHS_BUDGET, rhs.py:47).  Dense orders take
+ * part in ttagg_rhs / ttagg_rk2 like CP and TT orders (single GPU). */
+int ttagg_dense_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const double* values,
+                       ttagg_kernel** out);
 
 int ttagg_kernel_free(ttagg_kernel* k);
 

@@ -349,9 +349,46 @@ def ternary_case():
     save("ternary.npz", rows=np.array(series.rows()), n_final=final.n)
 
 
+def dense_case():
+    """Direct-summation operators rhs_dense_P / rhs_dense_Q (rhs.py:202-227) on
+    dense kernels the reference builds itself: a TableSpec read back from a
+    binary file (its dense input format), a Brownian spec materialized by
+    dense_from_spec, and a mixed KernelSet through rhs_total."""
+    import tempfile
+
+    from ttagg import DenseKernel, TableSpec, dense_from_spec, rhs_dense_P, rhs_dense_Q
+
+    rng = np.random.default_rng(7)
+    out = {}
+    cases = [("d2", 2, 200), ("d3", 3, 40), ("d4", 4, 14), ("d5", 5, 8)]
+    with tempfile.TemporaryDirectory() as tmp:
+        for tag, d, N in cases:
+            a = rng.random((N,) * d)
+            sym = sum(np.transpose(a, perm) for perm in __import__("itertools").permutations(range(d)))
+            path = os.path.join(tmp, f"{tag}.bin")
+            sym.astype("<f8").tofile(path)
+            k = dense_from_spec(TableSpec(path=path, dimension=d), N)
+            n = rng.random(N) * np.exp(-np.arange(N) / (N / 4))
+            out[f"{tag}_values"] = k.values
+            out[f"{tag}_n"] = n
+            out[f"{tag}_P"] = rhs_dense_P(k, ConcentrationState(n))
+            out[f"{tag}_Q"] = rhs_dense_Q(k, ConcentrationState(n))
+    N = 40
+    kb = dense_from_spec(BrownianSpec((0.2, -0.2, 0.1)), N)
+    n = np.exp(-np.arange(N) / 10.0)
+    out["brown3_values"] = kb.values
+    out["brown3_n"] = n
+    out["brown3_P"] = rhs_dense_P(kb, ConcentrationState(n))
+    out["brown3_Q"] = rhs_dense_Q(kb, ConcentrationState(n))
+    ks = KernelSet({2: DenseKernel(out["d2_values"][:N, :N].copy()), 3: kb})
+    r = rhs_total(ks, ConcentrationState(n), breakdown=True)
+    out["mix_p"], out["mix_q"], out["mix_s"] = r.p, r.q, r.s
+    save("dense.npz", **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["unit", "ternary", "c1", "c2", "c3", "c4", "c5"]
+    which = sys.argv[1:] or ["unit", "ternary", "c1", "c2", "c3", "c4", "c5", "dense"]
     for name in which:
         t0 = time.perf_counter()
         globals()[f"{name}_case" if not name.endswith("_case") else name]()

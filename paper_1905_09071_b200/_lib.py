@@ -43,6 +43,7 @@ TTAGG_WANT_P = 2
 TTAGG_WANT_Q = 4
 KIND_CP = 1
 KIND_TT = 2
+KIND_DENSE = 3
 
 _c_int64_p = ctypes.POINTER(ctypes.c_int64)
 _c_double_p = ctypes.POINTER(ctypes.c_double)
@@ -63,6 +64,10 @@ _SIGNATURES = {
     "ttagg_tt_upload": (
         ctypes.c_int,
         [_vp, ctypes.c_int, ctypes.c_int64, _c_int64_p, ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
+    ),
+    "ttagg_dense_upload": (
+        ctypes.c_int,
+        [_vp, ctypes.c_int, ctypes.c_int64, _vp, ctypes.POINTER(_vp)],
     ),
     "ttagg_kernel_free": (ctypes.c_int, [_vp]),
     "ttagg_kernel_info": (ctypes.c_int, [_vp, _c_int64_p]),
@@ -214,6 +219,15 @@ class Context:
         )
         return DeviceKernel(self, h, KIND_TT, d, n_classes)
 
+    def upload_dense(self, values) -> DeviceKernel:
+        lib = load()
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        d, n_classes = v.ndim, v.shape[0]
+        h = _vp()
+        check(lib.ttagg_dense_upload(self.handle, d, n_classes, v.ctypes.data, ctypes.byref(h)),
+              "ttagg_dense_upload")
+        return DeviceKernel(self, h, KIND_DENSE, d, n_classes)
+
     def device_kernel(self, kernel, rank_subset=None) -> DeviceKernel:
         """Upload once per (immutable) kernel object; cached by identity (kernels.py:129-134)."""
         key = (id(kernel), None if rank_subset is None else tuple(int(r) for r in rank_subset))
@@ -227,6 +241,10 @@ class Context:
                 if rank_subset is not None:
                     raise NotImplementedError("rank sharding of TT kernels")
                 dk = self.upload_tt(kernel.cores)
+            elif hasattr(kernel, "values"):
+                if rank_subset is not None:
+                    raise NotImplementedError("rank sharding of dense kernels")
+                dk = self.upload_dense(kernel.values)
             else:
                 from .kernels import KernelError
 

@@ -187,6 +187,10 @@ struct ttagg_kernel {
   int ntail = 0;
   int* tail_cols = nullptr;
   int nblk = 0;  // pass-A blocks per column (dot partials)
+  double* V = nullptr;     // dense: N^d coefficients, row-major (natural sizes)
+  double* nat = nullptr;   // dense: the state in natural order (scratch, N)
+  double* part = nullptr;  // dense: loss partial sums [chunks][N]
+  int chunks = 0;          // dense: loss chunks over the first d-1 modes
   int* fdesc = nullptr;  // TT: descriptors of the uploaded (live) fibers
   int* cidx = nullptr;   // TT: full fiber index -> uploaded column or -1
   int C_full = 0;        // TT: fibers before dropping
@@ -1037,6 +1041,104 @@ __global__ void permute_kernel(const double* __restrict__ in, double* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// dense kernels: direct summation (rhs.py:202-227), O(N^d) with N^d <= 2^26
+// ---------------------------------------------------------------------------
+struct DenseArgs {
+  const double* V;    // N^d, row-major
+  const double* nat;  // state in natural order
+  double* p_perm;     // gain (perm layout) or null
+  double* part;       // loss partials [chunks][N]
+  double* w_perm;     // loss contraction (perm layout)
+  int N, d, N1, N2, chunks;
+  long long head;     // N^(d-1)
+  double fact;        // d!
+};
+
+__device__ __forceinline__ size_t perm_of(long long o, int N1, int N2) {
+  return (size_t)(o % N2) * N1 + (size_t)(o / N2);
+}
+
+// state in natural order: n + alpha k rounded as numpy does (state_at)
+__global__ void dense_state_kernel(const double* nv, const double* kv, double alpha, double* nat, int N, int N1,
+                                   int N2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) nat[i] = state_at(nv, kv, alpha, perm_of(i, N1, N2));
+}
+
+__device__ __forceinline__ double block_sum_fixed(double v, double* red) {
+  // fixed-order block reduction (deterministic): warp trees, then warp 0
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+
+// Gain at output position o (size o+1): the tuples (i_1..i_d), 0-based, with
+// i_1 + ... + i_d = o - d + 1 (sizes summing to o + 1), weighted
+// C[i] n_{i_1} ... n_{i_d} in axis order (rhs.py:205-216); divided by d!.
+// One CTA per o; threads stride over the leading d-1 indices.
+__global__ void __launch_bounds__(256) dense_gain_kernel(const DenseArgs a) {
+  __shared__ double red[8];
+  const int o = blockIdx.x;
+  const int s = o - (a.d - 1);
+  double acc = 0.0;
+  if (s >= 0) {
+    for (long long m = threadIdx.x; m < a.head; m += blockDim.x) {
+      int idx[MAXD];
+      long long rem = m;
+      int sum = 0;
+      for (int j = a.d - 2; j >= 0; --j) {
+        idx[j] = (int)(rem % a.N);
+        rem /= a.N;
+        sum += idx[j];
+      }
+      const int last = s - sum;
+      if (last < 0 || last >= a.N) continue;
+      double w = __ldg(a.V + (size_t)m * a.N + last);
+      for (int j = 0; j < a.d - 1; ++j) w *= __ldg(a.nat + idx[j]);
+      w *= __ldg(a.nat + last);
+      acc += w;
+    }
+  }
+  const double tot = block_sum_fixed(acc, red);
+  if (threadIdx.x == 0) a.p_perm[perm_of(o, a.N1, a.N2)] = s >= 0 ? tot / a.fact : 0.0;
+}
+
+// Loss contraction w[k] = sum over the first d-1 modes of C[i_1..i_{d-1}, k]
+// n_{i_1}...n_{i_{d-1}} (rhs.py:219-227): per chunk of leading indices a
+// partial per k (coalesced over k), then a fixed-order sum over chunks.
+__global__ void __launch_bounds__(128) dense_loss_part_kernel(const DenseArgs a) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (a.head + a.chunks - 1) / a.chunks;
+  const long long m0 = (long long)blockIdx.y * per, m1 = min(a.head, m0 + per);
+  double acc = 0.0;
+  if (k < a.N) {
+    for (long long m = m0; m < m1; ++m) {
+      double u = 1.0;
+      long long rem = m;
+      for (int j = a.d - 2; j >= 0; --j) {
+        u *= __ldg(a.nat + (int)(rem % a.N));
+        rem /= a.N;
+      }
+      acc += __ldg(a.V + (size_t)m * a.N + k) * u;
+    }
+    a.part[(size_t)blockIdx.y * a.N + k] = acc;
+  }
+}
+
+__global__ void dense_loss_finish_kernel(const DenseArgs a) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.N) return;
+  double w = 0.0;
+  for (int c = 0; c < a.chunks; ++c) w += a.part[(size_t)c * a.N + k];
+  a.w_perm[perm_of(k, a.N1, a.N2)] = w;
+}
+
 // scatter an N x R row-major factor (or a TT core slice) into perm-layout columns:
 // column (rank index j) goes to column colmap[j] of X — pair-interleaved
 // (`paired`, the pass-A operand: column c at X[((c/2) Np + e) 2 + c%2]) or one
@@ -1426,7 +1528,53 @@ int check_set(const ttagg_kernel* const* ks, int nk, Geom* g) {
 }
 
 // Relative device cost of one order's gain (column count x transform length).
-double order_cost(const ttagg_kernel* k) { return (double)std::max(k->C_pad, 1) * k->plan->K_rows; }
+double order_cost(const ttagg_kernel* k) {
+  if (k->kind == TTAGG_KIND_DENSE) return 0.0;
+  return (double)std::max(k->C_pad, 1) * k->plan->K_rows;
+}
+
+// Dense order (rhs_dense_P / rhs_dense_Q): gain into p_perm, loss contraction
+// into the kernel's Xt (its single "tail" column, coefficient 1).
+int run_dense(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const double* kv, double alpha, double* p_perm,
+              bool wantQ, cudaStream_t st) {
+  const Geom& g = k->g;
+  const int N = (int)k->N;
+  dense_state_kernel<<<(N + 255) / 256, 256, 0, st>>>(nv, kv, alpha, k->nat, N, g.N1, g.N2);
+  CUDA_TRY(cudaGetLastError());
+  DenseArgs a{};
+  a.V = k->V;
+  a.nat = k->nat;
+  a.p_perm = p_perm;
+  a.part = k->part;
+  a.w_perm = k->Xt;
+  a.N = N;
+  a.d = k->d;
+  a.N1 = g.N1;
+  a.N2 = g.N2;
+  a.chunks = k->chunks;
+  long long head = 1;
+  for (int j = 0; j < k->d - 1; ++j) head *= N;
+  a.head = head;
+  double f = 1.0;
+  for (int i = 2; i <= k->d; ++i) f *= i;
+  a.fact = f;
+  ctx->launches += 1;
+  if (p_perm) {
+    ProfScope ps(ctx, 0, st, k->d);
+    dense_gain_kernel<<<N, 256, 0, st>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    ++ctx->launches;
+  }
+  if (wantQ) {
+    ProfScope ps(ctx, 3, st, k->d);
+    dense_loss_part_kernel<<<dim3((N + 127) / 128, k->chunks), 128, 0, st>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    dense_loss_finish_kernel<<<(N + 255) / 256, 256, 0, st>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches += 2;
+  }
+  return TTAGG_OK;
+}
 
 int make_streams(ttagg_ctx* ctx) {
   if (ctx->s_main) return TTAGG_OK;
@@ -1449,17 +1597,23 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
                double alpha, bool wantP, bool wantQ, CombineArgs* A, cudaStream_t st) {
   const Geom& g = ks[0]->g;
   if (wantP) TRY(ensure((void**)&ctx->pbuf, &ctx->pbuf_bytes, (size_t)nk * g.Np * sizeof(double)));
-  std::vector<int> order(nk);
-  for (int i = 0; i < nk; ++i) order[i] = i;
+  auto pslot = [&](int i) { return wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr; };
+  std::vector<int> order;  // FFT-route orders (CP / TT), costliest first
+  for (int i = 0; i < nk; ++i) {
+    if (ks[i]->kind == TTAGG_KIND_DENSE)
+      TRY(run_dense(ctx, ks[i], nv, kv, alpha, pslot(i), wantQ, st));
+    else
+      order.push_back(i);
+  }
   std::stable_sort(order.begin(), order.end(),
                    [&](int x, int y) { return order_cost(ks[x]) > order_cost(ks[y]); });
-  auto pslot = [&](int i) { return wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr; };
+  const int nf = (int)order.size();
   static int serial = -1;  // TTAGG_SERIAL=1: one stream (diagnostics)
   if (serial < 0) {
     const char* e = getenv("TTAGG_SERIAL");
     serial = e ? atoi(e) : 0;
   }
-  const bool conc = wantP && nk > 1 && !serial;
+  const bool conc = wantP && nf > 1 && !serial;
   if (!conc) {
     for (int i : order) {
       TRY(run_passA(ctx, ks[i], nv, kv, alpha, wantP, wantQ, ctx->work[i], st));
@@ -1471,13 +1625,13 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
     CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(ctx->s_main, ctx->ev_fork, 0));
     CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill, ctx->ev_fork, 0));
-    for (int n = nk - 1; n >= 1; --n)  // cheapest first: their pass B/C can start early
+    for (int n = nf - 1; n >= 1; --n)  // cheapest first: their pass B/C can start early
       TRY(run_passA(ctx, ks[order[n]], nv, kv, alpha, true, wantQ, ctx->work[order[n]], ctx->s_main));
     CUDA_TRY(cudaEventRecord(ctx->ev_a, ctx->s_main));
     TRY(run_passA(ctx, ks[big], nv, kv, alpha, true, wantQ, ctx->work[big], ctx->s_main));
     TRY(run_passBC(ctx, ks[big], pslot(big), ctx->work[big], ctx->s_main));
     CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill, ctx->ev_a, 0));
-    for (int n = 1; n < nk; ++n) TRY(run_passBC(ctx, ks[order[n]], pslot(order[n]), ctx->work[order[n]], ctx->s_fill));
+    for (int n = 1; n < nf; ++n) TRY(run_passBC(ctx, ks[order[n]], pslot(order[n]), ctx->work[order[n]], ctx->s_fill));
     CUDA_TRY(cudaEventRecord(ctx->ev_a, ctx->s_main));
     CUDA_TRY(cudaEventRecord(ctx->ev_fill, ctx->s_fill));
     CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_a, 0));
@@ -1839,6 +1993,50 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   return TTAGG_OK;
 }
 
+int ttagg_dense_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const double* values, ttagg_kernel** out) {
+  if (!ctx || !out || !values) return fail(TTAGG_ERR_ARG, "null argument");
+  if (d < 2) return fail(TTAGG_ERR_ARG, "dense kernels must have dimension >= 2");
+  if (d > MAXD) return fail(TTAGG_ERR_UNSUPPORTED, "collision order above 8");
+  int64_t total = 1;
+  for (int j = 0; j < d; ++j) {
+    total *= n_classes;
+    if (total > (int64_t(1) << 26))
+      return fail(TTAGG_ERR_UNSUPPORTED, "dense evaluation over the budget of 2^26 elements (rhs.py:47, 188-199)");
+  }
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  Geom g;
+  TRY(make_geom(n_classes, &g));
+  ttagg_kernel* k = new ttagg_kernel();
+  k->ctx = ctx;
+  k->kind = TTAGG_KIND_DENSE;
+  k->d = d;
+  k->N = n_classes;
+  k->g = g;
+  k->C = 0;
+  k->C_pad = 0;
+  k->R = 1;
+  const int64_t head = total / n_classes;
+  k->chunks = (int)std::max<int64_t>(1, std::min<int64_t>(head, 2048 / std::max<int64_t>(1, (n_classes + 127) / 128)));
+  CUDA_TRY(cudaMalloc(&k->V, (size_t)total * sizeof(double)));
+  CUDA_TRY(cudaMemcpy(k->V, values, (size_t)total * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&k->nat, (size_t)n_classes * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&k->part, (size_t)k->chunks * n_classes * sizeof(double)));
+  // the loss contraction is the order's single tail column (coefficient 1):
+  // the combine forms -(n w)/(d-1)! exactly as rhs.py:227
+  CUDA_TRY(cudaMalloc(&k->Xt, (size_t)g.Np * sizeof(double)));
+  CUDA_TRY(cudaMemset(k->Xt, 0, (size_t)g.Np * sizeof(double)));
+  const int zero = 0;
+  const double one = 1.0;
+  k->ntail = 1;
+  CUDA_TRY(cudaMalloc(&k->tail_cols, sizeof(int)));
+  CUDA_TRY(cudaMemcpy(k->tail_cols, &zero, sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&k->coef, sizeof(double)));
+  CUDA_TRY(cudaMemcpy(k->coef, &one, sizeof(double), cudaMemcpyHostToDevice));
+  *out = k;
+  return TTAGG_OK;
+}
+
 int ttagg_kernel_free(ttagg_kernel* k) {
   if (!k) return TTAGG_OK;
   cudaSetDevice(k->ctx->device);
@@ -1850,6 +2048,9 @@ int ttagg_kernel_free(ttagg_kernel* k) {
   cudaFree(k->coef);
   cudaFree(k->fdesc);
   cudaFree(k->cidx);
+  cudaFree(k->V);
+  cudaFree(k->nat);
+  cudaFree(k->part);
   delete k;
   return TTAGG_OK;
 }

@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["KernelError", "TTKernel", "CPKernel", "constant_cp", "constant_tt"]
+__all__ = ["KernelError", "TTKernel", "CPKernel", "DenseKernel", "constant_cp", "constant_tt"]
 
 
 class KernelError(ValueError):
@@ -115,3 +115,28 @@ def constant_cp(value: float, dimension: int, n_classes: int) -> CPKernel:
     factors = [np.ones((n_classes, 1)) for _ in range(dimension)]
     factors[0] = factors[0] * float(value)
     return CPKernel(tuple(factors))
+
+
+@dataclass(frozen=True, eq=False)
+class DenseKernel:
+    """Fully materialized kernel (kernels.py:218-238): N^d coefficients,
+    row-major, equal mode sizes; evaluated by direct summation."""
+
+    values: np.ndarray
+
+    def __post_init__(self):
+        values = _readonly(self.values)
+        if values.ndim < 2:
+            raise KernelError("dense kernels must have dimension >= 2")
+        n_classes = values.shape[0]
+        if any(s != n_classes for s in values.shape):
+            raise KernelError("dense kernels must have equal mode sizes")
+        object.__setattr__(self, "values", values)
+
+    @property
+    def dimension(self) -> int:
+        return self.values.ndim
+
+    @property
+    def n_classes(self) -> int:
+        return self.values.shape[0]

@@ -7,11 +7,12 @@ as the reference:
 * ``rhs_cp_Q(kernel, state, plan=None)``  — rhs.py:394-414
 * ``rhs_tt_P(kernel, state, plan=None)``  — rhs.py:234-302
 * ``rhs_tt_Q(kernel, state, plan=None)``  — rhs.py:321-338
+* ``rhs_dense_P(kernel, state)`` / ``rhs_dense_Q(kernel, state)`` — rhs.py:202-227
 * ``rhs_total(kernels, state, plan=None, *, breakdown=False)`` — rhs.py:421-459
 
 All arithmetic runs in the sm_100a CUDA extension (``libttagg_b200.so``);
 there is no CPU fallback.  Inputs may be this package's containers or the
-reference's own ``CPKernel`` / ``TTKernel`` / ``ConcentrationState`` /
+reference's own ``CPKernel`` / ``TTKernel`` / ``DenseKernel`` / ``ConcentrationState`` /
 ``KernelSet`` objects.  Outputs are fresh fp64 numpy arrays owned by the
 caller (rhs.py:296, 385, 459).
 """
@@ -24,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from ._lib import get_context
-from .kernels import CPKernel, KernelError, TTKernel
+from .kernels import CPKernel, DenseKernel, KernelError, TTKernel
 from .parallel import SERIAL_PLAN, ExecutionPlan
 
 __all__ = [
@@ -37,8 +38,13 @@ __all__ = [
     "rhs_tt_Q",
     "rhs_cp_P",
     "rhs_cp_Q",
+    "rhs_dense_P",
+    "rhs_dense_Q",
     "rhs_total",
+    "DENSE_RHS_BUDGET",
 ]
+
+DENSE_RHS_BUDGET = 1 << 26  # rhs.py:47
 
 _SYMMETRY_CHECK_MAX_N = 64
 _SYMMETRY_TOL = 1e-8
@@ -76,16 +82,24 @@ def _is_tt(k) -> bool:
     return hasattr(k, "cores")
 
 
+def _is_dense(k) -> bool:
+    return hasattr(k, "values") and not (_is_cp(k) or _is_tt(k))
+
+
 def _dimension(k) -> int:
+    if _is_dense(k):
+        return np.ndim(k.values)
     return len(k.factors) if _is_cp(k) else len(k.cores)
 
 
 def _n_classes(k) -> int:
+    if _is_dense(k):
+        return k.values.shape[0]
     return k.factors[0].shape[0] if _is_cp(k) else k.cores[0].shape[1]
 
 
 def kernel_element(kernel, idx) -> float:
-    """One coefficient of a CP or TT kernel (rhs.py:82-91; kernels.py:310-325)."""
+    """One coefficient of a CP, TT or dense kernel (rhs.py:80-91; kernels.py:310-325)."""
     entries = tuple(int(i) for i in idx)
     d = _dimension(kernel)
     if len(entries) != d:
@@ -100,6 +114,8 @@ def kernel_element(kernel, idx) -> float:
         for size, core in zip(entries[1:], kernel.cores[1:]):
             v = v @ core[:, size - 1, :]
         return float(v[0, 0])
+    if _is_dense(kernel):
+        return float(kernel.values[tuple(i - 1 for i in entries)])
     raise KernelError(f"unsupported kernel representation {type(kernel).__name__}")
 
 
@@ -131,7 +147,7 @@ class KernelSet:
             d = int(order)
             if d < 2:
                 raise KernelError(f"collision order must be >= 2, got {d}")
-            if not (_is_cp(kernel) or _is_tt(kernel)):
+            if not (_is_cp(kernel) or _is_tt(kernel) or _is_dense(kernel)):
                 raise KernelError(f"unsupported kernel representation {type(kernel).__name__}")
             if _dimension(kernel) != d:
                 raise KernelError(f"kernel for order {d} has dimension {_dimension(kernel)}")
@@ -188,9 +204,11 @@ def _check_pair(kernel, state) -> tuple:
 
 def _one(kernel, state, want_p: bool, want_q: bool, kind_ok, label: str):
     if not kind_ok(kernel):
-        raise KernelError(f"{label} needs a {'CP' if kind_ok is _is_cp else 'TT'} kernel, "
-                          f"got {type(kernel).__name__}")
-    _, n = _check_pair(kernel, state)
+        kind = {_is_cp: "CP", _is_tt: "TT", _is_dense: "dense"}[kind_ok]
+        raise KernelError(f"{label} needs a {kind} kernel, got {type(kernel).__name__}")
+    d, n = _check_pair(kernel, state)
+    if kind_ok is _is_dense:
+        _dense_budget_check(d, n.size)
     ctx = get_context()
     dk = ctx.device_kernel(kernel)
     out = ctx.rhs_host([dk], n, want_p=want_p, want_q=want_q,
@@ -216,6 +234,25 @@ def rhs_cp_P(kernel: CPKernel, state: ConcentrationState, plan: ExecutionPlan | 
 def rhs_cp_Q(kernel: CPKernel, state: ConcentrationState, plan: ExecutionPlan | None = None) -> np.ndarray:
     """Loss vector through a CP kernel (rhs.py:394-414), on the GPU."""
     return _one(kernel, state, False, True, _is_cp, "rhs_cp_Q")
+
+
+def _dense_budget_check(order: int, n_classes: int) -> None:
+    """rhs.py:188-199."""
+    if n_classes**order > DENSE_RHS_BUDGET:
+        raise KernelError(
+            f"dense evaluation needs {n_classes**order} elements, over the "
+            f"budget of {DENSE_RHS_BUDGET}; reduce N"
+        )
+
+
+def rhs_dense_P(kernel: DenseKernel, state: ConcentrationState) -> np.ndarray:
+    """Gain vector by direct summation over all d-tuples (rhs.py:202-216), on the GPU."""
+    return _one(kernel, state, True, False, _is_dense, "rhs_dense_P")
+
+
+def rhs_dense_Q(kernel: DenseKernel, state: ConcentrationState) -> np.ndarray:
+    """Loss vector by contracting the first d-1 modes with the state (rhs.py:219-227), on the GPU."""
+    return _one(kernel, state, False, True, _is_dense, "rhs_dense_Q")
 
 
 def _kernel_items(kernels):
@@ -244,11 +281,10 @@ def rhs_total(kernels: KernelSet, state: ConcentrationState, plan: ExecutionPlan
     if n_classes != n.size:
         raise KernelError(f"kernel set has N = {n_classes}, state has N = {n.size}")
     for d, k in items:
-        if not (_is_cp(k) or _is_tt(k)):
-            raise KernelError(
-                f"kernel for order {d} ({type(k).__name__}) is not a CP or TT kernel; "
-                "dense kernels are outside the GPU path"
-            )
+        if not (_is_cp(k) or _is_tt(k) or _is_dense(k)):
+            raise KernelError(f"unsupported kernel representation {type(k).__name__}")
+        if _is_dense(k):
+            _dense_budget_check(d, n.size)
     ctx = get_context()
     dks = [ctx.device_kernel(k) for _, k in items]
     if not breakdown:

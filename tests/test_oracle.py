@@ -252,3 +252,13 @@ def test_c3_literal_failure_and_normalised_trajectory(golden):
                                  steps=cfg.steps, record_every=20)
     assert rel_inf(n, g["norm4096_n_final"]) <= 1e-11
     np.testing.assert_allclose(np.array(series.rows()), g["norm4096_rows"], rtol=1e-10, atol=1e-18)
+
+
+@pytest.mark.parametrize("tag", ["d2", "d3", "d4", "d5", "brown3"])
+def test_dense_oracle_vs_reference(golden, tag):
+    """Direct-summation operators (rhs.py:202-227) on the reference's own dense
+    kernels (TableSpec file, dense Brownian), against its outputs."""
+    g = golden("dense.npz")
+    v, n = g[f"{tag}_values"], g[f"{tag}_n"]
+    assert rel_inf(orc.dense_gain(v, n), g[f"{tag}_P"]) <= 1e-12
+    assert rel_inf(orc.dense_loss(v, n), g[f"{tag}_Q"]) <= 1e-12
