@@ -192,10 +192,27 @@ def test_install_patches_reference_seams():
     import ttagg.integrator as ti
     import ttagg.rhs as tr
 
-    before = (tr.rhs_cp_P, ti.rhs_total)
+    before = (tr.rhs_cp_P, tr.rhs_dense_P, tr.rhs_dense_Q, ti.rhs_total)
     undo = g.install(ttagg)
     try:
-        assert tr.rhs_cp_P is g.rhs_cp_P and ti.rhs_total is not before[1]
+        assert tr.rhs_cp_P is g.rhs_cp_P and ti.rhs_total is not before[3]
+        assert tr.rhs_dense_P is g.rhs_dense_P and tr.rhs_dense_Q is g.rhs_dense_Q
     finally:
         undo()
-    assert (tr.rhs_cp_P, ti.rhs_total) == before
+    assert (tr.rhs_cp_P, tr.rhs_dense_P, tr.rhs_dense_Q, ti.rhs_total) == before
+
+
+def test_dense_kernel_container_and_budget():
+    """DenseKernel validation (kernels.py:218-238) and the dense budget
+    (rhs.py:188-199) are host-side: no GPU needed."""
+    with pytest.raises(g.KernelError):
+        g.DenseKernel(np.ones(5))
+    with pytest.raises(g.KernelError):
+        g.DenseKernel(np.ones((4, 5)))
+    k = g.DenseKernel(np.arange(27.0).reshape(3, 3, 3))
+    assert k.dimension == 3 and k.n_classes == 3
+    assert g.kernel_element(k, (1, 2, 3)) == 5.0
+    with pytest.raises(g.KernelError, match="budget"):
+        g.rhs_dense_P(g.DenseKernel(np.zeros((8193, 8193))), g.ConcentrationState(np.ones(8193)))
+    with pytest.raises(g.KernelError, match="budget"):
+        g.rhs_total(g.KernelSet({2: g.DenseKernel(np.zeros((8193, 8193)))}), g.ConcentrationState(np.ones(8193)))
