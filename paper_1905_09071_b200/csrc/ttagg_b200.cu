@@ -479,7 +479,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // over the 8 rows fastest so every warp load reads whole 128-byte segments
 // of the P and M planes T[pair][plane][n2][rho]; the row transforms exchange
 // through shared memory.  Per column pair: FFT(P row), FFT(M row), then the
-// two real columns separate in registers: A = (P + M)/2, B = -i (P - M)/2.
+// two real columns separate in registers: 2A = P + M, 2B = -i (P - M).
 // The next pair's planes stream in with cp.async while this pair computes:
 // every thread copies exactly the elements it later reads, into two staging
 // regions that double as the row FFTs' exchange buffers (P stage for FFT(P),
