@@ -160,3 +160,45 @@ def test_dist_engine_rk2_matches_fused_integrate():
     assert res.fail_step == 0
     assert rel_inf(res.n, final.n) <= 1e-13
     assert_rows(res.rows, series.rows(), 1e-12)
+
+
+def test_dt_halving_ratio_is_second_order():
+    """test_integrator.py:105-110 / test_acceptance.py:157-165: halving dt cuts
+    the RK2 error by ~4 (reference solution at dt/8)."""
+    N = 256
+    ks = g.KernelSet({3: g.constant_tt(1.0, 3, N)})
+    n0 = initial_state("mono", N)
+    T = 0.4
+
+    def final(dt):
+        return g.integrate(Cfg(n0, dt, int(round(T / dt)), int(round(T / dt))), kernels=ks)[0].n
+
+    ref = final(0.0125)
+    e1 = np.abs(final(0.1) - ref).max()
+    e2 = np.abs(final(0.05) - ref).max()
+    assert 3.2 <= e1 / e2 <= 4.8
+
+
+def test_brownian_tt_mass_drift():
+    """test_integrator.py:130-141: the exact Brownian TT kernel conserves mass
+    to <= 1e-6 over 100 steps at N = 1024 before boundary contact (here through
+    the live-fiber TT upload)."""
+    from test_gpu_tt_sparse import subset_tt
+
+    N = 1024
+    ks = g.KernelSet({3: g.TTKernel(subset_tt((0.1, -0.1, 0.0), N))})
+    n0 = initial_state("mono", N)
+    final, series = g.integrate(Cfg(n0, 1e-3, 100, 100), kernels=ks)
+    m1 = np.array([r[2] for r in series.rows()])
+    assert abs(m1[-1] - m1[0]) / m1[0] <= 1e-6
+
+
+def test_execution_plan_does_not_change_results():
+    """test_rhs.py:330-366 (worker-count and FFT-length-policy independence):
+    the GPU path accepts any plan; results are bitwise identical."""
+    cfg = CONFIGS["C1"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    st = g.ConcentrationState(initial_state("exp256", cfg.n_classes))
+    base = g.rhs_total(ks, st).s
+    for plan in (g.ExecutionPlan(workers=8), g.ExecutionPlan(fft_length_policy="min"), g.SERIAL_PLAN):
+        assert np.array_equal(g.rhs_total(ks, st, plan).s, base)
