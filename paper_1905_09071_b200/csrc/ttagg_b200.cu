@@ -1309,6 +1309,8 @@ int launchB(const PassBArgs& a, int grid, cudaStream_t st) {
 
 int rowsB(int N2) { return 128 / fft_t(N2); }
 
+// N2 <= 256 always (make_geom): the row block is 8 rows of one 16-thread
+// row transform each (the lane map in passB_kernel assumes T <= 16)
 int dispatchB(int N2, bool tt, const PassBArgs& a, int grid, cudaStream_t st) {
 #define TTAGG_B(n) \
   case n: return tt ? launchB<n, true>(a, grid, st) : launchB<n, false>(a, grid, st);
@@ -1318,7 +1320,6 @@ int dispatchB(int N2, bool tt, const PassBArgs& a, int grid, cudaStream_t st) {
     TTAGG_B(64)
     TTAGG_B(128)
     TTAGG_B(256)
-    TTAGG_B(512)
   }
 #undef TTAGG_B
   return fail(TTAGG_ERR_UNSUPPORTED, "unsupported N2");
