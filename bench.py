@@ -184,6 +184,46 @@ def run_reference(args, N, factors_by_order, n0):
     print(json.dumps(line), flush=True)
 
 
+def c4_tt_timing(ctx, N, dev, stream, steps):
+    """RHS/s of config C4's shape: d = 3 TT with ranks (1, 16, 16, 1) (the
+    rank cap of the TT-cross kernel; seeded random cores stand in for the
+    8-minute host compression — the cost depends on the ranks only) and the
+    exact rank-3 TT of (i^(1/3) + j^(1/3))^2 for d = 2, monodisperse state."""
+    import numpy as np
+    import torch
+
+    import paper_1905_09071_b200 as g
+
+    rng = np.random.default_rng(0)
+    i = np.arange(1, N + 1, dtype=np.float64)
+    c1 = np.stack([i ** (2 / 3), 2 * i ** (1 / 3), np.ones(N)], axis=1)[None]
+    c2 = np.stack([np.ones(N), i ** (1 / 3), i ** (2 / 3)], axis=0)[:, :, None]
+    r = 16
+    d3 = (rng.random((1, N, r)), rng.random((r, N, r)) / r, rng.random((r, N, 1)))
+    ks = g.KernelSet({2: g.TTKernel((c1, c2)), 3: g.TTKernel(d3)})
+    del d3
+    dks = [ctx.device_kernel(ks[d]) for d in ks.orders]
+    n = torch.zeros(N, dtype=torch.float64, device=dev)
+    n[0] = 1.0
+    p = torch.empty_like(n)
+    q = torch.empty_like(n)
+    s = torch.empty_like(n)
+    sp = stream.cuda_stream
+    for _ in range(3):
+        ctx.rhs_device(dks, n.data_ptr(), p.data_ptr(), q.data_ptr(), s.data_ptr(), sp)
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        ctx.rhs_device(dks, n.data_ptr(), p.data_ptr(), q.data_ptr(), s.data_ptr(), sp)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b) / steps
+    return {"ms_per_rhs": ms, "rhs_per_s": 1000.0 / ms, "unit": UNIT,
+            "workload": "config C4 shape: D=3, N=2^20, TT d=3 ranks (1,16,16,1) seeded cores + exact d=2 rank-3 TT, fp64",
+            "note": "CUDA events on the launching stream, inputs resident"}
+
+
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
@@ -196,6 +236,7 @@ def main():
     ap.add_argument("--n-classes", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the D=3 TT (config C4 shape) RHS timing")
     ap.add_argument("--rk2-steps", type=int, default=50)  # config C5: dt = 0.002, 50 steps
     ap.add_argument("--sharded", action="store_true",
                     help="use the rank-sharded multi-GPU code path (perm layout + all-reduce) even at 1 GPU")
@@ -341,6 +382,11 @@ def main():
                    "d2h_bytes_per_step": 8 * N, "api": "ttagg_rhs_perm + NCCL all-reduce (pinned host buffers)"}
 
     # ---- RK2 steps/s (fused device-resident integrator), single GPU
+    # ---- D = 3 at N = 2^20 through the TT route (config C4 shape), single GPU
+    c4 = None
+    if not sharded and not args.no_c4 and N == 1 << 20:
+        c4 = c4_tt_timing(ctx, N, dev, stream, args.steps)
+
     rk2 = None
     if not sharded and args.rk2_steps > 0:
         nn = initial_state("c5", N, normalised=True)
@@ -417,6 +463,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "rk2": rk2,
+        "c4_tt": c4,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
