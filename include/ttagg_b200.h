@@ -73,7 +73,9 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank,
 /* Upload a TT kernel (replaces TTKernel, kernels.py:137-180, plus the fiber
  * layout of rhs_tt_P, rhs.py:256-269).  ranks: d+1 entries with
  * ranks[0] == ranks[d] == 1; cores: d host pointers, core l of shape
- * (ranks[l], N, ranks[l+1]) row-major. */
+ * (ranks[l], N, ranks[l+1]) row-major.  Only live fibers are uploaded:
+ * identically zero fibers and fibers on chain paths that are zero add
+ * nothing to the gain or the loss and are dropped. */
 int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ranks,
                     const double* const* cores, ttagg_kernel** out);
 
@@ -87,7 +89,7 @@ int ttagg_dense_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const double* v
 
 int ttagg_kernel_free(ttagg_kernel* k);
 
-/* info[0]=kind, [1]=d, [2]=N, [3]=columns (CP d*R_local / TT fibers),
+/* info[0]=kind, [1]=d, [2]=N, [3]=columns (CP d*R_local / TT live fibers / dense 0),
  * [4]=Np, [5]=N1, [6]=N2, [7]=rows per column in the exchange */
 int ttagg_kernel_info(const ttagg_kernel* k, int64_t* info8);
 
