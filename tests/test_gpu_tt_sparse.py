@@ -108,3 +108,21 @@ def test_subset_tt_set_matches_cp_set_in_total():
     b = g.rhs_total(ks_cp, st(n))
     assert rel_inf(a.s, b.s) <= TOL
     assert math.isfinite(float(np.abs(a.s).max()))
+
+
+@pytest.mark.parametrize("ranks", [(1, 64, 1), (1, 3, 64, 2, 1), (1, 64, 64, 1)])
+def test_tt_max_ranks_vs_oracle(ranks):
+    """The largest TT ranks the build takes (64): chain state and loss chain."""
+    n_classes = 3000
+    rng = np.random.default_rng(sum(ranks))
+    cores = tuple(rng.random((ranks[l], n_classes, ranks[l + 1])) / ranks[l] for l in range(len(ranks) - 1))
+    n = rng.random(n_classes)
+    k = g.TTKernel(cores)
+    assert rel_inf(g.rhs_tt_P(k, st(n)), orc.tt_gain(cores, n)) <= TOL
+    assert rel_inf(g.rhs_tt_Q(k, st(n)), orc.tt_loss(cores, n)) <= TOL
+
+
+def test_tt_rank_above_64_is_rejected():
+    cores = (np.ones((1, 16, 65)), np.ones((65, 16, 1)))
+    with pytest.raises(Exception, match="64"):
+        g.rhs_tt_P(g.TTKernel(cores), st(np.ones(16)))
