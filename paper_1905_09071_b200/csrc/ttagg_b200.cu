@@ -1751,6 +1751,29 @@ int ttagg_ctx_destroy(ttagg_ctx* ctx) {
   return TTAGG_OK;
 }
 
+// Frees a kernel's device buffers (cudaFree(nullptr) is a no-op) and the
+// handle; upload failures release a partially built kernel through
+// KernelGuard, so no error path leaks device memory.
+static void release_kernel(ttagg_kernel* k) {
+  if (!k) return;
+  cudaSetDevice(k->ctx->device);
+  cudaDeviceSynchronize();
+  for (void* p : {(void*)k->X, (void*)k->Xt, (void*)k->tail_cols, (void*)k->dots, (void*)k->coef, (void*)k->fdesc,
+                  (void*)k->cidx, (void*)k->V, (void*)k->nat, (void*)k->part})
+    cudaFree(p);
+  delete k;
+}
+
+struct KernelGuard {
+  ttagg_kernel* k;
+  ~KernelGuard() { release_kernel(k); }
+  ttagg_kernel* release() {
+    ttagg_kernel* r = k;
+    k = nullptr;
+    return r;
+  }
+};
+
 static int finish_upload(ttagg_ctx* ctx, ttagg_kernel* k, const std::vector<int>& tails) {
   k->ntail = (int)tails.size();
   CUDA_TRY(cudaMalloc(&k->tail_cols, std::max<size_t>(1, tails.size()) * sizeof(int)));
@@ -1783,6 +1806,7 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
     for (int64_t r = 0; r < rank; ++r) sel.push_back((int)r);
   }
   ttagg_kernel* k = new ttagg_kernel();
+  KernelGuard guard{k};
   k->ctx = ctx;
   k->kind = TTAGG_KIND_CP;
   k->d = d;
@@ -1796,7 +1820,6 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
   {
     cudaError_t e = cudaMalloc(&k->X, std::max<size_t>(2, k->C_pad) * colbytes);
     if (e != cudaSuccess) {
-      delete k;
       return fail(TTAGG_ERR_NOMEM, "factor upload allocation failed");
     }
   }
@@ -1834,7 +1857,7 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
     for (int j = 0; j < k->R; ++j) tails.push_back(j);  // rows of Xt
   }
   TRY(finish_upload(ctx, k, tails));
-  *out = k;
+  *out = guard.release();
   return TTAGG_OK;
 }
 
@@ -1851,6 +1874,7 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   Geom g;
   TRY(make_geom(n_classes, &g));
   ttagg_kernel* k = new ttagg_kernel();
+  KernelGuard guard{k};
   k->ctx = ctx;
   k->kind = TTAGG_KIND_TT;
   k->d = d;
@@ -1862,7 +1886,6 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
     Rmax = std::max(Rmax, (int)ranks[l]);
   }
   if (Rmax > 64) {
-    delete k;
     return fail(TTAGG_ERR_UNSUPPORTED, "TT ranks above 64");
   }
   for (int l = 0; l < d; ++l) {
@@ -1873,7 +1896,6 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   k->C_full = C;
   for (int l = 0; l < d; ++l)
     if (!cores[l]) {
-      delete k;
       return fail(TTAGG_ERR_ARG, "null core");
     }
   // Live fibers.  A fiber H_l[rp, :, rn] that is identically zero adds nothing
@@ -1990,7 +2012,7 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   std::vector<int> tails;
   for (int rp = 0; rp < k->ranks[d - 1]; ++rp) tails.push_back(rp);  // rows of Xt
   TRY(finish_upload(ctx, k, tails));
-  *out = k;
+  *out = guard.release();
   return TTAGG_OK;
 }
 
@@ -2009,6 +2031,7 @@ int ttagg_dense_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const double* v
   Geom g;
   TRY(make_geom(n_classes, &g));
   ttagg_kernel* k = new ttagg_kernel();
+  KernelGuard guard{k};
   k->ctx = ctx;
   k->kind = TTAGG_KIND_DENSE;
   k->d = d;
@@ -2034,25 +2057,12 @@ int ttagg_dense_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const double* v
   CUDA_TRY(cudaMemcpy(k->tail_cols, &zero, sizeof(int), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMalloc(&k->coef, sizeof(double)));
   CUDA_TRY(cudaMemcpy(k->coef, &one, sizeof(double), cudaMemcpyHostToDevice));
-  *out = k;
+  *out = guard.release();
   return TTAGG_OK;
 }
 
 int ttagg_kernel_free(ttagg_kernel* k) {
-  if (!k) return TTAGG_OK;
-  cudaSetDevice(k->ctx->device);
-  cudaDeviceSynchronize();
-  cudaFree(k->X);
-  cudaFree(k->Xt);
-  cudaFree(k->tail_cols);
-  cudaFree(k->dots);
-  cudaFree(k->coef);
-  cudaFree(k->fdesc);
-  cudaFree(k->cidx);
-  cudaFree(k->V);
-  cudaFree(k->nat);
-  cudaFree(k->part);
-  delete k;
+  release_kernel(k);
   return TTAGG_OK;
 }
 
