@@ -356,3 +356,21 @@ def test_workspace_regrowth_between_kernel_sets():
     ref = orc.rhs_total({d: {"kind": "cp", "arrays": big[d].factors} for d in big.orders}, n)
     assert rel_inf(got.p, ref[0]) <= TOL
     assert rel_inf(got.s, ref[2]) <= TOL
+
+
+@pytest.mark.parametrize("n_classes", [300001, 600000])
+def test_large_ragged_sizes_vs_oracle(n_classes):
+    """Ragged N in the 2048- and 4096-point column-transform geometries
+    (N1 = 2048 at N = 300001, N1 = 4096 at N = 600000), every order, CP and TT."""
+    rng = np.random.default_rng(n_classes)
+    n = rng.random(n_classes) * np.exp(-np.arange(n_classes) / (n_classes / 8))
+    for d in (2, 3, 4, 5):
+        fs = tuple(rng.random((n_classes, 2)) for _ in range(d))
+        k = g.CPKernel(fs)
+        assert rel_inf(g.rhs_cp_P(k, st(n)), orc.cp_gain(fs, n)) <= TOL
+        assert rel_inf(g.rhs_cp_Q(k, st(n)), orc.cp_loss(fs, n)) <= TOL
+    ranks = (1, 3, 2, 1)
+    cores = tuple(rng.random((ranks[l], n_classes, ranks[l + 1])) for l in range(3))
+    kt = g.TTKernel(cores)
+    assert rel_inf(g.rhs_tt_P(kt, st(n)), orc.tt_gain(cores, n)) <= TOL
+    assert rel_inf(g.rhs_tt_Q(kt, st(n)), orc.tt_loss(cores, n)) <= TOL
