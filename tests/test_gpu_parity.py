@@ -374,3 +374,22 @@ def test_large_ragged_sizes_vs_oracle(n_classes):
     kt = g.TTKernel(cores)
     assert rel_inf(g.rhs_tt_P(kt, st(n)), orc.tt_gain(cores, n)) <= TOL
     assert rel_inf(g.rhs_tt_Q(kt, st(n)), orc.tt_loss(cores, n)) <= TOL
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+@pytest.mark.parametrize("n_classes", [8, 16, 32])
+def test_acceptance_criterion_2_small_sizes(order, n_classes):
+    """test_acceptance.py:79-106: fast paths vs the dense direct sums for
+    d in {2,3,4} x N in {8,16,32} x 20 states, CP and TT, P and Q, 1e-10."""
+    rng = np.random.default_rng(100 * order + n_classes)
+    fs = tuple(rng.random((n_classes, 3)) for _ in range(order))
+    ranks = (1,) + (2,) * (order - 1) + (1,)
+    cores = tuple(rng.random((ranks[l], n_classes, ranks[l + 1])) for l in range(order))
+    kc, kt = g.CPKernel(fs), g.TTKernel(cores)
+    dc, dt = orc.dense_from_cp(fs), orc.dense_from_tt(cores)
+    for _ in range(20):
+        n = rng.random(n_classes)
+        assert rel_inf(g.rhs_cp_P(kc, st(n)), orc.dense_gain(dc, n)) <= TOL
+        assert rel_inf(g.rhs_cp_Q(kc, st(n)), orc.dense_loss(dc, n)) <= TOL
+        assert rel_inf(g.rhs_tt_P(kt, st(n)), orc.dense_gain(dt, n)) <= TOL
+        assert rel_inf(g.rhs_tt_Q(kt, st(n)), orc.dense_loss(dt, n)) <= TOL
