@@ -299,6 +299,44 @@ def c5_case():
     save("c5.npz", **out)
 
 
+def c5traj_case():
+    """The C5 trajectory at full size: N = 2^20, D = 5, dt = 0.002, 50 steps,
+    on the mass-normalised state (the literal one diverges at step 2, SURVEY.md
+    §8(d)), through the reference's own integrate() on its Brownian TT route
+    (the same tensor as the permutation-power CP kernels; the CP route needs
+    more memory than this container has).  Stored: sample indices of the
+    final state, full-vector checksums and the moment rows (every 10 steps)."""
+    cfg = CONFIGS["C5"]
+    n_classes = cfg.n_classes
+    ks_tt = KernelSet(
+        {d: build_brownian_tt(BrownianSpec(cfg.exponents[:d]), n_classes) for d in cfg.orders}
+    )
+    n0 = initial_state("c5", n_classes, normalised=True)
+    t0 = time.perf_counter()
+    traj = _run_traj(ks_tt, n0, cfg.dt, cfg.steps, 10)
+    print(f"C5 full-N trajectory {time.perf_counter() - t0:.1f}s", flush=True)
+    idx = sample_indices(n_classes)
+    save("c5traj.npz", idx=idx, n_final=traj["n_final"][idx], n_sums=checksums(traj["n_final"]),
+         rows=traj["rows"], fail_step=traj["fail_step"], negativity=traj["negativity"], warned=traj["warned"])
+
+
+def c3traj_case():
+    """The C3 trajectory at full size: N = 2^18, D = 4, dt = 0.005, 200 steps,
+    mass-normalised state (the literal one diverges at step 2), through the
+    reference's own integrate() on its CP route.  Stored: sample indices of
+    the final state, full-vector checksums and the moment rows (every 20)."""
+    cfg = CONFIGS["C3"]
+    n_classes = cfg.n_classes
+    ks = cp_set(cfg.cp_factors())
+    n0 = initial_state("exp256", n_classes, normalised=True)
+    t0 = time.perf_counter()
+    traj = _run_traj(ks, n0, cfg.dt, cfg.steps, 20)
+    print(f"C3 full-N trajectory {time.perf_counter() - t0:.1f}s", flush=True)
+    idx = sample_indices(n_classes)
+    save("c3traj.npz", idx=idx, n_final=traj["n_final"][idx], n_sums=checksums(traj["n_final"]),
+         rows=traj["rows"], fail_step=traj["fail_step"], negativity=traj["negativity"], warned=traj["warned"])
+
+
 def c4_case():
     """C4-shaped TT case at a size where the dense TT-SVD is cheap.
 

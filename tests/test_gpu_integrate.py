@@ -202,3 +202,40 @@ def test_execution_plan_does_not_change_results():
     base = g.rhs_total(ks, st).s
     for plan in (g.ExecutionPlan(workers=8), g.ExecutionPlan(fft_length_policy="min"), g.SERIAL_PLAN):
         assert np.array_equal(g.rhs_total(ks, st, plan).s, base)
+
+
+def test_c5_full_size_trajectory_vs_reference(golden):
+    """North star: the RK2 trajectory at N = 2^20, D = 5 (config C5: dt = 0.002,
+    50 steps; mass-normalised state since the literal one diverges at step 2)
+    against the reference's own integrate() on the same tensor (its Brownian
+    TT route) — sampled final state, full-vector checksums, moment rows —
+    to the north star's 1e-8."""
+    c = golden("c5traj.npz")
+    cfg = CONFIGS["C5"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    n0 = initial_state("c5", cfg.n_classes, normalised=True)
+    final, series = g.integrate(Cfg(n0, cfg.dt, cfg.steps, 10), kernels=ks)
+    assert int(c["fail_step"]) == 0
+    assert rel_inf(final.n[c["idx"]], c["n_final"]) <= TRAJ_TOL
+    k = np.arange(1, cfg.n_classes + 1, dtype=np.float64)
+    v = final.n
+    sums = np.array([v.sum(), k @ v, (k * k) @ v, np.abs(v).sum(), np.abs(v).max()])
+    assert np.all(np.abs(sums - c["n_sums"]) <= TRAJ_TOL * np.abs(c["n_sums"]))
+    assert_rows(series.rows(), c["rows"], TRAJ_TOL)
+
+
+def test_c3_full_size_trajectory_vs_reference(golden):
+    """Config C3 at full size (N = 2^18, D = 4, dt = 0.005, 200 steps,
+    mass-normalised state) against the reference's own integrate() (CP route)."""
+    c = golden("c3traj.npz")
+    cfg = CONFIGS["C3"]
+    ks = g.KernelSet({d: g.CPKernel(f) for d, f in cfg.cp_factors().items()})
+    n0 = initial_state("exp256", cfg.n_classes, normalised=True)
+    final, series = g.integrate(Cfg(n0, cfg.dt, cfg.steps, 20), kernels=ks)
+    assert int(c["fail_step"]) == 0
+    assert rel_inf(final.n[c["idx"]], c["n_final"]) <= TRAJ_TOL
+    k = np.arange(1, cfg.n_classes + 1, dtype=np.float64)
+    v = final.n
+    sums = np.array([v.sum(), k @ v, (k * k) @ v, np.abs(v).sum(), np.abs(v).max()])
+    assert np.all(np.abs(sums - c["n_sums"]) <= TRAJ_TOL * np.abs(c["n_sums"]))
+    assert_rows(series.rows(), c["rows"], TRAJ_TOL)
