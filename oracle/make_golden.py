@@ -337,6 +337,35 @@ def c3traj_case():
          rows=traj["rows"], fail_step=traj["fail_step"], negativity=traj["negativity"], warned=traj["warned"])
 
 
+def c4traj_case():
+    """Config C4 at full size: N = 2^20, D = 3, TT kernels (exact rank-3 d = 2,
+    TT-cross d = 3 with ranks 16 from paper_1905_09071_b200.construct, the
+    compressor the reference lacks), monodisperse state, dt = 0.01, 100
+    steps, through the reference's own integrate() on its TT route.  The d = 3
+    cores are 2 GB, so the fixture stores the cross skeleton (I, J) that
+    rebuilds them (construct.c4_d3_from_skeleton), the sampled final state,
+    checksums and the moment rows (every 10 steps)."""
+    from paper_1905_09071_b200 import construct
+
+    n_classes = 1 << 20
+    t0 = time.perf_counter()
+    (c1, c2), cores3, (I, J) = construct.c4_kernels(n_classes, rank=16, return_skeleton=True)
+    print(f"C4 cross {time.perf_counter() - t0:.1f}s ranks {[c.shape[2] for c in cores3]}", flush=True)
+    ks = KernelSet({2: TTKernel((c1, c2)), 3: TTKernel(tuple(cores3))})
+    n0 = np.zeros(n_classes)
+    n0[0] = 1.0
+    t0 = time.perf_counter()
+    traj = _run_traj(ks, n0, 0.01, 100, 10)
+    print(f"C4 full-N trajectory {time.perf_counter() - t0:.1f}s", flush=True)
+    idx = sample_indices(n_classes)
+    out = dict(idx=idx, n_final=traj["n_final"][idx], n_sums=checksums(traj["n_final"]), rows=traj["rows"],
+               fail_step=traj["fail_step"], negativity=traj["negativity"], warned=traj["warned"])
+    for k in range(3):  # I[0..d-1] and J[1..d] define the d = 3 cores
+        out[f"I{k}"] = I[k]
+        out[f"J{k + 1}"] = J[k + 1]
+    save("c4traj.npz", **out)
+
+
 def c4_case():
     """C4-shaped TT case at a size where the dense TT-SVD is cheap.
 

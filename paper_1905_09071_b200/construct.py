@@ -16,7 +16,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["maxvol", "tt_cross", "c4_kernels", "tt_rank_shard"]
+__all__ = ["maxvol", "tt_cross", "cores_from_skeleton", "c4_kernels", "c4_d2_cores", "c4_d3_from_skeleton",
+           "tt_rank_shard"]
 
 
 def _orth(a: np.ndarray) -> np.ndarray:
@@ -56,23 +57,8 @@ def maxvol(a: np.ndarray, tol: float = 1.05, max_iters: int = 64) -> np.ndarray:
     return idx
 
 
-def tt_cross(f, n_classes: int, d: int, rank: int, sweeps: int = 2, seed: int = 0):
-    """TT-cross with fixed ranks (1, r, ..., r, 1) of f(idx) on [1..N]^d.
-
-    ``f(points)`` evaluates the function on an (m, d) array of 1-based
-    indices.  Returns d cores of shape (r_{k-1}, N, r_k).
-    """
-    rng = np.random.default_rng(seed)
-    N = n_classes
-    r = [1] + [min(rank, N ** min(k, d - k)) for k in range(1, d)] + [1]
+def _fiber_fn(f, N: int, d: int):
     grid = np.arange(1, N + 1)
-    # left index sets I[k]: (r[k], k) multi-indices; right sets J[k]: (r[k], d-k)
-    J = [None] * (d + 1)
-    J[d] = np.zeros((1, 0), dtype=np.int64)
-    for k in range(d - 1, 0, -1):
-        J[k] = rng.integers(1, N + 1, size=(r[k], d - k))
-    I = [None] * (d + 1)
-    I[0] = np.zeros((1, 0), dtype=np.int64)
 
     def fiber(k, Ik, Jk1):
         # tensor of values f(I_k, i, J_{k+1}) with shape (r_k, N, r_{k+1})
@@ -85,7 +71,52 @@ def tt_cross(f, n_classes: int, d: int, rank: int, sweeps: int = 2, seed: int = 
         pts[:, :, :, k + 1 :] = Jk1[None, None, :, :]
         return f(pts.reshape(-1, d)).reshape(a, N, b)
 
+    return fiber
+
+
+def cores_from_skeleton(f, n_classes: int, d: int, I, J):
+    """TT cores of f through the cross skeleton (left index sets I[0..d-1],
+    right index sets J[1..d]): C_k = f(I_k, :, J_{k+1}) times the inverse of
+    f(I_{k+1}, J_{k+1}).  A few seconds at N = 2^20 — the skeleton (a few KB)
+    is what fixtures store instead of the cores."""
+    fiber = _fiber_fn(f, n_classes, d)
     cores = [None] * d
+    for k in range(d):
+        c = fiber(k, I[k], J[k + 1])
+        if k < d - 1:
+            r0, r1 = c.shape[0], c.shape[2]
+            cmat = c.reshape(r0 * n_classes, r1)
+            a = I[k + 1].shape[0]
+            full = np.empty((a, J[k + 1].shape[0], d), dtype=np.int64)
+            full[:, :, : k + 1] = I[k + 1][:, None, :]
+            full[:, :, k + 1 :] = J[k + 1][None, :, :]
+            m = f(full.reshape(-1, d)).reshape(a, -1)
+            cmat = np.linalg.solve(m.T, cmat.T).T
+            cores[k] = np.ascontiguousarray(cmat.reshape(r0, n_classes, r1))
+        else:
+            cores[k] = np.ascontiguousarray(c)
+    return cores
+
+
+def tt_cross(f, n_classes: int, d: int, rank: int, sweeps: int = 2, seed: int = 0, return_skeleton: bool = False):
+    """TT-cross with fixed ranks (1, r, ..., r, 1) of f(idx) on [1..N]^d.
+
+    ``f(points)`` evaluates the function on an (m, d) array of 1-based
+    indices.  Returns d cores of shape (r_{k-1}, N, r_k) (and, with
+    ``return_skeleton``, the index sets I, J that determine them).
+    """
+    rng = np.random.default_rng(seed)
+    N = n_classes
+    r = [1] + [min(rank, N ** min(k, d - k)) for k in range(1, d)] + [1]
+    grid = np.arange(1, N + 1)
+    # left index sets I[k]: (r[k], k) multi-indices; right sets J[k]: (r[k], d-k)
+    J = [None] * (d + 1)
+    J[d] = np.zeros((1, 0), dtype=np.int64)
+    for k in range(d - 1, 0, -1):
+        J[k] = rng.integers(1, N + 1, size=(r[k], d - k))
+    I = [None] * (d + 1)
+    I[0] = np.zeros((1, 0), dtype=np.int64)
+    fiber = _fiber_fn(f, N, d)
     for _ in range(sweeps):
         # left-to-right: choose I[k+1]
         for k in range(d - 1):
@@ -101,23 +132,8 @@ def tt_cross(f, n_classes: int, d: int, rank: int, sweeps: int = 2, seed: int = 
                 [np.repeat(grid, r[k + 1])[:, None], np.tile(J[k + 1], (N, 1))], axis=1
             )
             J[k] = right[sel]
-    # cores: C_k = f(I_k, :, J_{k+1}) times the inverse of f(I_{k+1}, J_{k+1}) on the right
-    for k in range(d):
-        c = fiber(k, I[k], J[k + 1])
-        if k < d - 1:
-            cmat = c.reshape(r[k] * N, r[k + 1])
-            pts = np.concatenate([I[k + 1], J[k + 1]], axis=1)  # (r_{k+1}, d)
-            # skeleton matrix f(I_{k+1}, J_{k+1}) as (r_{k+1} x r_{k+1}) with rows = I, cols = J
-            a = I[k + 1].shape[0]
-            full = np.empty((a, J[k + 1].shape[0], d), dtype=np.int64)
-            full[:, :, : k + 1] = I[k + 1][:, None, :]
-            full[:, :, k + 1 :] = J[k + 1][None, :, :]
-            m = f(full.reshape(-1, d)).reshape(a, -1)
-            cmat = np.linalg.solve(m.T, cmat.T).T
-            cores[k] = np.ascontiguousarray(cmat.reshape(r[k], N, r[k + 1]))
-        else:
-            cores[k] = np.ascontiguousarray(c)
-    return cores
+    cores = cores_from_skeleton(f, N, d, I, J)
+    return (cores, I, J) if return_skeleton else cores
 
 
 class _C4d3:
@@ -145,16 +161,30 @@ class _C4d3:
 _c4_d3 = _C4d3()
 
 
-def c4_kernels(n_classes: int, rank: int = 16, seed: int = 0):
-    """Config 4: {2: exact rank-3 TT of (i^(1/3)+j^(1/3))^2, 3: TT-cross of
-    (i+j+l)^(1/2)(ijl)^(-1/6) with ranks <= rank}; returns (cores2, cores3)."""
+def c4_d2_cores(n_classes: int):
+    """Exact rank-3 TT of (i^(1/3)+j^(1/3))^2 (config 4, d = 2)."""
     i = np.arange(1, n_classes + 1, dtype=np.float64)
     c1 = np.zeros((1, n_classes, 3))
     c1[0, :, 0], c1[0, :, 1], c1[0, :, 2] = i ** (2 / 3), 2 * i ** (1 / 3), 1.0
     c2 = np.zeros((3, n_classes, 1))
     c2[0, :, 0], c2[1, :, 0], c2[2, :, 0] = 1.0, i ** (1 / 3), i ** (2 / 3)
-    cores3 = tt_cross(_c4_d3, n_classes, 3, rank, seed=seed)
-    return (c1, c2), tuple(cores3)
+    return c1, c2
+
+
+def c4_kernels(n_classes: int, rank: int = 16, seed: int = 0, return_skeleton: bool = False):
+    """Config 4: {2: exact rank-3 TT of (i^(1/3)+j^(1/3))^2, 3: TT-cross of
+    (i+j+l)^(1/2)(ijl)^(-1/6) with ranks <= rank}; returns (cores2, cores3)
+    (and the d = 3 cross skeleton (I, J) with ``return_skeleton``)."""
+    out = tt_cross(_c4_d3, n_classes, 3, rank, seed=seed, return_skeleton=return_skeleton)
+    if return_skeleton:
+        cores3, I, J = out
+        return c4_d2_cores(n_classes), tuple(cores3), (I, J)
+    return c4_d2_cores(n_classes), tuple(out)
+
+
+def c4_d3_from_skeleton(n_classes: int, I, J):
+    """The config-4 d = 3 cores from a stored cross skeleton."""
+    return tuple(cores_from_skeleton(_c4_d3, n_classes, 3, I, J))
 
 
 def tt_rank_shard(cores, world: int, rank: int):

@@ -59,3 +59,13 @@ def test_tt_rank_shards_sum_to_full_rhs():
         l = sum(orc.tt_loss(p, n) for p in parts)
         assert rel_inf(g, full_g) <= 1e-13
         assert rel_inf(l, full_l) <= 1e-13
+
+
+def test_cross_skeleton_reproduces_cores():
+    """The stored skeleton (I, J) rebuilds the cross cores bit for bit."""
+    from paper_1905_09071_b200 import construct
+
+    (c1, c2), cores3, (I, J) = construct.c4_kernels(300, rank=6, return_skeleton=True)
+    again = construct.c4_d3_from_skeleton(300, I, J)
+    for a, b in zip(cores3, again):
+        assert np.array_equal(a, b)
