@@ -340,26 +340,40 @@ def c3traj_case():
 def c4traj_case():
     """Config C4 at full size: N = 2^20, D = 3, TT kernels (exact rank-3 d = 2,
     TT-cross d = 3 with ranks 16 from paper_1905_09071_b200.construct, the
-    compressor the reference lacks), monodisperse state, dt = 0.01, 100
-    steps, through the reference's own integrate() on its TT route.  The d = 3
+    compressor the reference lacks), monodisperse state, dt = 0.01, through
+    the reference's own integrate() on its TT route.  As literally specified
+    (100 steps) it diverges: StepSizeWarning, then StepFailureError at step 9
+    (explicit RK2 is unstable for the large sizes, whose loss rates reach
+    dt * 4 k^(2/3) >> 1; FFT roundoff there grows every step).  Stored: the
+    literal failure semantics, and a 2-step trajectory (record every step)
+    whose final state is compared at sampled sizes plus checksums.  The d = 3
     cores are 2 GB, so the fixture stores the cross skeleton (I, J) that
-    rebuilds them (construct.c4_d3_from_skeleton), the sampled final state,
-    checksums and the moment rows (every 10 steps)."""
+    rebuilds them (construct.c4_d3_from_skeleton)."""
     from paper_1905_09071_b200 import construct
 
     n_classes = 1 << 20
+    path = os.path.join(OUT, "c4traj.npz")
     t0 = time.perf_counter()
-    (c1, c2), cores3, (I, J) = construct.c4_kernels(n_classes, rank=16, return_skeleton=True)
-    print(f"C4 cross {time.perf_counter() - t0:.1f}s ranks {[c.shape[2] for c in cores3]}", flush=True)
+    if os.path.exists(path):  # reuse the skeleton of an earlier run (the cross takes minutes)
+        old = np.load(path)
+        I = [old["I0"], old["I1"], old["I2"]]
+        J = [None, old["J1"], old["J2"], old["J3"]]
+        cores3 = construct.c4_d3_from_skeleton(n_classes, I, J)
+    else:
+        _, cores3, (I, J) = construct.c4_kernels(n_classes, rank=16, return_skeleton=True)
+    c1, c2 = construct.c4_d2_cores(n_classes)
+    print(f"C4 cores {time.perf_counter() - t0:.1f}s ranks {[c.shape[2] for c in cores3]}", flush=True)
     ks = KernelSet({2: TTKernel((c1, c2)), 3: TTKernel(tuple(cores3))})
     n0 = np.zeros(n_classes)
     n0[0] = 1.0
-    t0 = time.perf_counter()
-    traj = _run_traj(ks, n0, 0.01, 100, 10)
-    print(f"C4 full-N trajectory {time.perf_counter() - t0:.1f}s", flush=True)
+    lit = _run_traj(ks, n0, 0.01, 100, 10)
+    short = _run_traj(ks, n0, 0.01, 2, 1)
+    print(f"C4 literal: fail_step {int(lit['fail_step'])} warned {bool(lit['warned'])}; "
+          f"2-step rows\n{short['rows']}", flush=True)
     idx = sample_indices(n_classes)
-    out = dict(idx=idx, n_final=traj["n_final"][idx], n_sums=checksums(traj["n_final"]), rows=traj["rows"],
-               fail_step=traj["fail_step"], negativity=traj["negativity"], warned=traj["warned"])
+    nf = short["n_final"]
+    out = dict(idx=idx, lit_fail_step=lit["fail_step"], lit_rows=lit["rows"], lit_warned=lit["warned"],
+               n2_final=nf[idx], n2_sums=checksums(nf), n2_rows=short["rows"])
     for k in range(3):  # I[0..d-1] and J[1..d] define the d = 3 cores
         out[f"I{k}"] = I[k]
         out[f"J{k + 1}"] = J[k + 1]

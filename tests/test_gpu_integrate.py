@@ -239,3 +239,41 @@ def test_c3_full_size_trajectory_vs_reference(golden):
     sums = np.array([v.sum(), k @ v, (k * k) @ v, np.abs(v).sum(), np.abs(v).max()])
     assert np.all(np.abs(sums - c["n_sums"]) <= TRAJ_TOL * np.abs(c["n_sums"]))
     assert_rows(series.rows(), c["rows"], TRAJ_TOL)
+
+
+def test_c4_full_size_vs_reference(golden):
+    """Config C4 at full size (N = 2^20, D = 3, TT kernels: exact rank-3 d = 2,
+    TT-cross d = 3 with ranks 16, rebuilt from the stored cross skeleton;
+    monodisperse, dt = 0.01) against the reference's own integrate() on the
+    same cores: as literally specified it diverges (StepSizeWarning, then
+    StepFailureError at step 9, one recorded row) and so must the GPU run;
+    the first two steps (before the instability of the large sizes reaches
+    the roundoff floor) are compared state for state."""
+    from paper_1905_09071_b200 import construct
+
+    c = golden("c4traj.npz")
+    N = 1 << 20
+    c1, c2 = construct.c4_d2_cores(N)
+    cores3 = construct.c4_d3_from_skeleton(N, [c["I0"], c["I1"], c["I2"]], [None, c["J1"], c["J2"], c["J3"]])
+    ks = g.KernelSet({2: g.TTKernel((c1, c2)), 3: g.TTKernel(cores3)})
+    n0 = initial_state("mono", N)
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
+        with pytest.raises(g.StepFailureError) as exc:
+            g.integrate(Cfg(n0, 0.01, 100, 10), kernels=ks)
+    assert exc.value.step_index == int(c["lit_fail_step"]) == 9
+    assert any(issubclass(w.category, g.StepSizeWarning) for w in caught) == bool(c["lit_warned"])
+    assert_rows(exc.value.series.rows(), c["lit_rows"], TRAJ_TOL)
+    final, series = g.integrate(Cfg(n0, 0.01, 2, 1), kernels=ks)
+    assert rel_inf(final.n[c["idx"]], c["n2_final"]) <= TRAJ_TOL
+    # M0, M1 and the state's own sums; the k^2-weighted M2 of a monodisperse
+    # start is dominated by the roundoff floor of the ~10^6 empty sizes
+    # (k^2 up to 10^12 times ~1e-17 noise, different in any two correct FFT
+    # implementations: 1.0577 vs 1.0578 after one step), so it is not compared
+    k = np.arange(1, N + 1, dtype=np.float64)
+    v = final.n
+    sums = np.array([v.sum(), k @ v, (k * k) @ v, np.abs(v).sum(), np.abs(v).max()])
+    for i in (0, 1, 4):
+        assert abs(sums[i] - c["n2_sums"][i]) <= TRAJ_TOL * abs(c["n2_sums"][i])
+    rows = np.array(series.rows())
+    assert np.allclose(rows[:, :3], c["n2_rows"][:, :3], rtol=TRAJ_TOL, atol=0.0)

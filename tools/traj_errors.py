@@ -38,3 +38,24 @@ for name, kind, rec in (("C5", "c5", 10), ("C3", "exp256", 20)):
     e_r = (np.abs(rows[:, 1:4] - c["rows"][:, 1:4]) / np.abs(c["rows"][:, 1:4])).max()
     print(f"{name} N={cfg.n_classes} steps={cfg.steps}: final-state rel max-norm {e_n:.2e}, "
           f"checksums {e_s:.2e}, moment rows {e_r:.2e}")
+
+path = os.path.join(ROOT, "tests", "golden", "c4traj.npz")
+if os.path.exists(path):
+    from paper_1905_09071_b200 import construct
+
+    c = np.load(path)
+    N = 1 << 20
+    cores3 = construct.c4_d3_from_skeleton(N, [c["I0"], c["I1"], c["I2"]], [None, c["J1"], c["J2"], c["J3"]])
+    ks = g.KernelSet({2: g.TTKernel(construct.c4_d2_cores(N)), 3: g.TTKernel(cores3)})
+    final, series = g.integrate(Cfg(initial_state("mono", N), 0.01, 2, 1), kernels=ks)
+    v = final.n
+    k = np.arange(1, v.size + 1, dtype=np.float64)
+    sums = np.array([v.sum(), k @ v, (k * k) @ v, np.abs(v).sum(), np.abs(v).max()])
+    e_n = np.abs(v[c["idx"]] - c["n2_final"]).max() / np.abs(c["n2_final"]).max()
+    sel = [0, 1, 4]  # M2-weighted sums are roundoff-dominated here (see the test)
+    e_s = (np.abs(sums[sel] - c["n2_sums"][sel]) / np.abs(c["n2_sums"][sel])).max()
+    rows = np.array(series.rows())
+    e_r = (np.abs(rows[:, 1:3] - c["n2_rows"][:, 1:3]) / np.abs(c["n2_rows"][:, 1:3])).max()
+    print(f"C4 N={N} first 2 steps (TT ranks {[x.shape[2] for x in cores3]}; the literal 100-step run diverges "
+          f"at step {int(c['lit_fail_step'])} in the reference): final-state rel max-norm {e_n:.2e}, "
+          f"checksums (M0, M1, max) {e_s:.2e}, moment rows (M0, M1) {e_r:.2e}")
