@@ -68,9 +68,15 @@ def launches(path, tag, command):
     names = [short(r["Kernel Name"]) for r in rows]
     # last complete device RHS (rhs_device): permute -> pass A ... -> combine_natural
     ends = [i for i, n in enumerate(names) if n.startswith("combine_natural")]
-    starts = [i for i, n in enumerate(names)
-              if n.startswith("permute") and i < ends[-1] and names[i + 1].startswith("passA")]
-    seg = rows[starts[-1]: ends[-1] + 1]
+    starts = [i for i, n in enumerate(names) if n.startswith("permute") and names[i + 1].startswith("passA")]
+    segs = []  # complete C5 RHS evaluations (the order-5 pass A has 300 pairs x N2 CTAs)
+    for a in starts:
+        b = next((e for e in ends if e > a), None)
+        if b is not None and any(names[i].startswith("passA") and grid_count(rows[i]["Grid Size"]) == 300 * N2
+                                 for i in range(a, b)):
+            segs.append((a, b))
+    a, b = segs[-1]
+    seg = rows[a: b + 1]
     labs = label([(r["Kernel Name"], grid_count(r["Grid Size"])) for r in seg])
     ns = [float(r["Metric Value"]) for r in seg]
     tot = sum(ns)
