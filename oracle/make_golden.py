@@ -467,6 +467,38 @@ def dense_case():
     save("dense.npz", **out)
 
 
+CLI_CONFIG = {
+    "N": 4096,
+    "D": 3,
+    "kernels": {"2": {"type": "brownian", "mu": [0.3, -0.3]},
+                "3": {"type": "brownian", "mu": [0.2, -0.1, -0.1]}},
+    "initial": {"kind": "monodisperse", "c0": 1.0},
+    "time": {"t0": 0.0, "dt": 0.01, "steps": 40},
+    "record_every": 10,
+}
+
+
+def cli_case():
+    """The reference's own CLI (``ttagg simulate``, cli.py:80-110) on a
+    Brownian D = 3 config: its moments.csv rows and the final snapshot
+    n_40.csv.  The kernels are the reference's default ones for Brownian
+    specs (exact TT, config.py:231-242)."""
+    import json
+    import tempfile
+
+    from ttagg import cli
+
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "run.json")
+        with open(path, "w") as fh:
+            json.dump(CLI_CONFIG, fh)
+        out = os.path.join(tmp, "out")
+        assert cli.main(["simulate", "--config", path, "--output", out]) == 0
+        rows = np.loadtxt(os.path.join(out, "moments.csv"), delimiter=",", skiprows=1)
+        snap = np.loadtxt(os.path.join(out, "n_40.csv"), delimiter=",", skiprows=1)
+    save("cli.npz", config=np.array(json.dumps(CLI_CONFIG)), rows=rows, n_final=snap[:, 1])
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     which = sys.argv[1:] or ["unit", "ternary", "c1", "c2", "c3", "c4", "c5", "dense"]

@@ -79,28 +79,49 @@ def install(ttagg_module=None):
     """Route an imported reference package through the GPU operators.
 
     Patches the reference's own call-time lookups:
-    ``ttagg.rhs.rhs_{cp,tt}_{P,Q}`` (used by its ``rhs_total``,
-    rhs.py:446-451) and ``ttagg.integrator.rhs_total`` (used by its
-    ``rk2_step``, integrator.py:16, 171), and the dense operators
-    ``ttagg.rhs.rhs_dense_{P,Q}``.  Returns a function that undoes the patch.
+
+    * ``ttagg.rhs.rhs_{cp,tt,dense}_{P,Q}`` (used by its ``rhs_total``,
+      rhs.py:446-451);
+    * ``ttagg.integrator.rhs_total`` (used by its ``rk2_step``,
+      integrator.py:16, 171);
+    * ``ttagg.integrator.integrate`` / ``ttagg.integrate`` and the name the
+      CLI bound at import, ``ttagg.cli.integrate`` (cli.py:21, 102): the
+      fused device RK2 (state resident, one CUDA graph per step).  Its
+      ``run_scaling_benchmark`` imports ``integrate`` lazily from the
+      integrator module (parallel.py:221-222) and picks the patch up too.
+      Results come back as the reference's own types (ConcentrationState,
+      MomentSeries, StepFailureError, StepSizeWarning), so the CLI's exit
+      codes and CSV writers work unchanged.
+
+    Returns a function that undoes the patch.
     """
     import importlib
+    import warnings as _warnings
 
+    from . import integrator as _integ
     from . import rhs as _rhs
 
     mod = ttagg_module or importlib.import_module("ttagg")
     rhs_mod = importlib.import_module(mod.__name__ + ".rhs")
     integ_mod = importlib.import_module(mod.__name__ + ".integrator")
-    saved = {
-        (rhs_mod, name): getattr(rhs_mod, name)
-        for name in ("rhs_cp_P", "rhs_cp_Q", "rhs_tt_P", "rhs_tt_Q", "rhs_dense_P", "rhs_dense_Q")
-    }
+    try:
+        cli_mod = importlib.import_module(mod.__name__ + ".cli")
+    except ImportError:
+        cli_mod = None
+    ops = ("rhs_cp_P", "rhs_cp_Q", "rhs_tt_P", "rhs_tt_Q", "rhs_dense_P", "rhs_dense_Q")
+    saved = {(rhs_mod, name): getattr(rhs_mod, name) for name in ops}
     saved[(integ_mod, "rhs_total")] = integ_mod.rhs_total
-    for name in ("rhs_cp_P", "rhs_cp_Q", "rhs_tt_P", "rhs_tt_Q", "rhs_dense_P", "rhs_dense_Q"):
+    saved[(integ_mod, "integrate")] = integ_mod.integrate
+    if hasattr(mod, "integrate"):
+        saved[(mod, "integrate")] = mod.integrate
+    if cli_mod is not None and hasattr(cli_mod, "integrate"):
+        saved[(cli_mod, "integrate")] = cli_mod.integrate
+    for name in ops:
         setattr(rhs_mod, name, getattr(_rhs, name))
 
     ref_total = rhs_mod.rhs_total
     ref_result = rhs_mod.RhsResult
+    ref_state = rhs_mod.ConcentrationState
 
     def gpu_total(kernels, state, plan=None, *, breakdown=False):
         ks = [kernels[d] for d in kernels.orders]
@@ -109,7 +130,43 @@ def install(ttagg_module=None):
             return ref_result(p=r.p, q=r.q, s=r.s, by_order=r.by_order)
         return ref_total(kernels, state, plan, breakdown=breakdown)
 
+    def to_ref_series(series):
+        if series is None:
+            return None
+        out = integ_mod.MomentSeries()
+        for name in ("times", "m0", "m1", "m2", "min_n", "m1_drift"):
+            setattr(out, name, list(getattr(series, name)))
+        out.negativity_flagged = series.negativity_flagged
+        return out
+
+    def gpu_integrate(config, kernels=None, plan=None, on_record=None):
+        cb = None
+        if on_record is not None:
+            def cb(step, state):
+                on_record(step, ref_state(state.n, state.t))
+        with _warnings.catch_warnings(record=True) as caught:
+            _warnings.simplefilter("always")
+            try:
+                final, series = _integ.integrate(config, kernels, plan, cb)
+            except _integ.StepFailureError as exc:
+                err = integ_mod.StepFailureError(str(exc), step_index=exc.step_index,
+                                                 series=to_ref_series(exc.series))
+                failure = err
+            else:
+                failure = None
+        for w in caught:  # re-issued as the reference's own warning classes
+            cat = integ_mod.StepSizeWarning if issubclass(w.category, _integ.StepSizeWarning) else w.category
+            _warnings.warn(str(w.message), cat, stacklevel=2)
+        if failure is not None:
+            raise failure
+        return ref_state(final.n, final.t), to_ref_series(series)
+
     integ_mod.rhs_total = gpu_total
+    integ_mod.integrate = gpu_integrate
+    if (mod, "integrate") in saved:
+        mod.integrate = gpu_integrate
+    if (cli_mod, "integrate") in saved:
+        cli_mod.integrate = gpu_integrate
 
     def uninstall():
         for (m, name), fn in saved.items():

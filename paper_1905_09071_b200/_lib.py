@@ -269,31 +269,14 @@ class Context:
         except Exception:
             return [np.empty(N) for _ in range(count)]
 
-    def _stage_input(self, n: np.ndarray) -> np.ndarray:
-        """Copy the state into a reused page-locked buffer (the H2D copy then
-        runs at full PCIe speed); large states are copied by a few host
-        threads in parallel (numpy releases the GIL)."""
-        buf = getattr(self, "_in_pinned", None)
-        if buf is None or buf.size < n.size:
-            buf = self._pinned(max(n.size, 1), 1)[0]
-            self._in_pinned = buf
-        view = buf[: n.size]
-        parts = _copy_parts(n.size)
-        if parts == 1:
-            np.copyto(view, n)
-        else:
-            bounds = np.linspace(0, n.size, parts + 1).astype(np.int64)
-            list(_copy_pool().map(lambda i: np.copyto(view[bounds[i]:bounds[i + 1]], n[bounds[i]:bounds[i + 1]]),
-                                  range(parts)))
-        return view
-
     def rhs_host(self, dkernels, n: np.ndarray, want_p=True, want_q=True, outputs=("p", "q", "s")):
         """Host-pointer RHS: returns dict of fresh numpy arrays."""
         lib = load()
         n = np.ascontiguousarray(n, dtype=np.float64)
         N = n.size
+        # outputs land in page-locked memory (DMA target, no extra host copy);
+        # the state is staged by the library itself (one call, no GIL hand-offs)
         if N >= 1 << 16:
-            n = self._stage_input(n)
             res = dict(zip(outputs, self._pinned(N, len(outputs))))
         else:
             res = {name: np.empty(N) for name in outputs}
@@ -377,22 +360,6 @@ class Context:
 
 
 _CONTEXTS: dict[int, Context] = {}
-_POOL = None
-
-
-def _copy_parts(size: int) -> int:
-    return 1 if size < (1 << 19) else min(4, os.cpu_count() or 1)
-
-
-def _copy_pool():
-    global _POOL
-    if _POOL is None:
-        with _LOCK:
-            if _POOL is None:
-                from concurrent.futures import ThreadPoolExecutor
-
-                _POOL = ThreadPoolExecutor(max_workers=4, thread_name_prefix="ttagg-stage")
-    return _POOL
 
 
 def get_context(device: int | None = None) -> Context:

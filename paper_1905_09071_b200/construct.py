@@ -7,6 +7,11 @@
   every implementation, so RHS parity never depends on the approximation.
 * ``c4_kernels`` — the C4 kernel set: exact rank-3 TT for (i^(1/3)+j^(1/3))^2
   (d = 2) and the cross-approximated d = 3 kernel (ranks <= 16, tol 1e-6).
+* ``brownian_tt`` / ``kernel_set_from_config`` — the reference's default
+  kernels for a ``SimulationConfig`` (config.py:231-242): the exact
+  constructive TT of a generalized Brownian kernel (Theorem 1,
+  kernels.py:332-363; ranks C(D, lam)), rank-1 constant TT, dense tables;
+  restated here so ``integrate(config)`` needs no reference import.
 * ``tt_rank_shard`` — slice a TT kernel over its first internal rank index:
   the gain and loss are linear in that index (rhs.py:277-290, 305-338), so
   the slices of all GPUs sum to the full RHS (TT rank sharding).
@@ -17,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["maxvol", "tt_cross", "cores_from_skeleton", "c4_kernels", "c4_d2_cores", "c4_d3_from_skeleton",
-           "tt_rank_shard"]
+           "tt_rank_shard", "brownian_tt", "kernel_set_from_config"]
 
 
 def _orth(a: np.ndarray) -> np.ndarray:
@@ -197,3 +202,87 @@ def tt_rank_shard(cores, world: int, rank: int):
     out[0] = np.ascontiguousarray(cores[0][:, :, sel])
     out[1] = np.ascontiguousarray(cores[1][sel, :, :])
     return tuple(out)
+
+
+# ---------------------------------------------------------------------------
+# default kernels of a SimulationConfig (config.py:231-242)
+# ---------------------------------------------------------------------------
+
+def _colex_subsets(d: int, level: int):
+    """level-subsets of the labels 1..d in colexicographic order (kernels.py:266-287)."""
+    from itertools import combinations
+
+    return sorted(combinations(range(1, d + 1), level), key=lambda t: t[::-1])
+
+
+def brownian_tt(exponents, n_classes: int):
+    """Exact TT cores of the generalized Brownian kernel with exponents mu
+    (Theorem 1; the construction of build_brownian_tt, kernels.py:332-363).
+
+    Rank index r at level lam is the r-th lam-subset S of the exponent labels
+    (colex order); the fiber S -> T of core lam is the power vector
+    i^mu_l = exp(mu_l log i) of the one label l = T \\ S when S is contained
+    in T, and zero otherwise.  Ranks C(D, lam)."""
+    mus = [float(m) for m in exponents]
+    d = len(mus)
+    if d < 2:
+        raise ValueError("a Brownian kernel needs at least two exponents")
+    sizes = np.arange(1, n_classes + 1, dtype=np.float64)
+    logs = np.log(sizes)
+    pows = [np.exp(mu * logs) for mu in mus]
+    levels = [_colex_subsets(d, lam) for lam in range(d + 1)]
+    index = [{sub: r for r, sub in enumerate(lv)} for lv in levels]
+    cores = []
+    for lam in range(1, d + 1):
+        core = np.zeros((len(levels[lam - 1]), n_classes, len(levels[lam])))
+        for rc, T in enumerate(levels[lam]):
+            for label in T:
+                S = tuple(x for x in T if x != label)
+                core[index[lam - 1][S], :, rc] = pows[label - 1]
+        cores.append(core)
+    return tuple(cores)
+
+
+def _load_table(path: str, d: int, n_classes: int) -> np.ndarray:
+    """N^d coefficients, flat little-endian binary or text (kernels.py:404-422)."""
+    import os
+
+    from .kernels import KernelError
+
+    expected = n_classes ** d
+    if not os.path.exists(path):
+        raise KernelError(f"kernel table file not found: {path}")
+    if os.path.getsize(path) == expected * 8:
+        flat = np.fromfile(path, dtype="<f8")
+    else:
+        try:
+            flat = np.loadtxt(path, dtype=np.float64).ravel()
+        except (ValueError, UnicodeDecodeError) as exc:
+            raise KernelError(f"kernel table {path} could not be read ({exc})") from None
+    if flat.size != expected:
+        raise KernelError(f"kernel table {path} holds {flat.size} values, expected {expected}")
+    return flat.reshape((n_classes,) * d)
+
+
+def kernel_set_from_config(config):
+    """KernelSet of a config's ``kernel_specs`` exactly as the reference's
+    build_kernel_set (config.py:231-242): Brownian specs -> exact TT,
+    constant specs -> rank-1 TT, tables -> dense.  Specs are recognised by
+    their fields (``exponents`` / ``value`` / ``path``)."""
+    from .kernels import DenseKernel, KernelError, TTKernel, constant_tt
+    from .rhs import KernelSet
+
+    N = int(config.n_classes)
+    out = {}
+    for d, spec in config.kernel_specs.items():
+        if hasattr(spec, "exponents"):
+            out[d] = TTKernel(brownian_tt(spec.exponents, N))
+        elif hasattr(spec, "value"):
+            out[d] = constant_tt(spec.value, d, N)
+        elif hasattr(spec, "path"):
+            if N ** d > 1 << 26:
+                raise KernelError(f"dense kernel would hold {N ** d} elements, over the budget of {1 << 26}")
+            out[d] = DenseKernel(_load_table(spec.path, spec.dimension, N))
+        else:
+            raise KernelError(f"unsupported kernel specification {type(spec).__name__}")
+    return KernelSet(out)

@@ -40,6 +40,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fft.cuh"
@@ -170,6 +171,14 @@ struct ttagg_ctx {
   std::vector<Rec> recs;
   double prof_acc[5] = {0, 0, 0, 0, 0};
   long long launches = 0;  // kernel launches issued by this context
+  // the workspaces above are shared by every call: the GPU work of a call
+  // issued on one stream waits for the previous call's (on any other stream)
+  cudaEvent_t ev_last = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool last_valid = false;
+  // page-locked staging for host-pointer calls whose buffers are pageable
+  double* pin = nullptr;
+  size_t pin_bytes = 0;
 };
 
 struct ttagg_kernel {
@@ -1231,14 +1240,17 @@ int get_plan(ttagg_ctx* ctx, int d, const Geom& g, OrderPlan** out) {
   return TTAGG_OK;
 }
 
-// raise the dynamic shared-memory cap once per kernel instantiation (never
-// inside a stream capture: the first launch of every shape runs eagerly)
+// raise the dynamic shared-memory cap once per (device, kernel instantiation):
+// cudaFuncSetAttribute applies to the current device only (never inside a
+// stream capture: the first launch of every shape runs eagerly)
 template <typename K>
 int set_smem(K kern, size_t bytes) {
   static std::mutex mu;
-  static std::map<const void*, size_t> done;  // per kernel instantiation
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
-  size_t& have = done[(const void*)kern];
+  size_t& have = done[std::make_pair(dev, (const void*)kern)];
   if (bytes > 48 * 1024 && bytes > have) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     have = bytes;
@@ -1588,6 +1600,72 @@ int make_streams(ttagg_ctx* ctx) {
   return TTAGG_OK;
 }
 
+// host memory the driver can DMA directly (cudaHostAlloc / cudaHostRegister)
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// memcpy split over a few host threads for large vectors (pageable <-> pinned)
+void par_copy(void* dst, const void* src, size_t bytes) {
+  const size_t min_part = size_t(1) << 21;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int parts = (int)std::min<size_t>(std::min<unsigned>(8u, hw), std::max<size_t>(1, bytes / min_part));
+  if (parts <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t chunk = (bytes / parts + 63) & ~size_t(63);
+  std::vector<std::thread> th;
+  for (int i = 1; i < parts; ++i) {
+    const size_t off = std::min(bytes, chunk * i), end = std::min(bytes, off + chunk);
+    if (end > off) th.emplace_back([=] { std::memcpy((char*)dst + off, (const char*)src + off, end - off); });
+  }
+  std::memcpy(dst, src, std::min(bytes, chunk));
+  for (auto& t : th) t.join();
+}
+
+int ensure_pinned(ttagg_ctx* ctx, size_t need) {
+  if (ctx->pin_bytes >= need) return TTAGG_OK;
+  if (ctx->pin) cudaFreeHost(ctx->pin);
+  ctx->pin = nullptr;
+  ctx->pin_bytes = 0;
+  CUDA_TRY(cudaHostAlloc((void**)&ctx->pin, need, cudaHostAllocDefault));
+  ctx->pin_bytes = need;
+  return TTAGG_OK;
+}
+
+// Calls on a context share its workspaces (exchange, vectors, diagnostics):
+// a call's stream first waits for the previous call's last operation when
+// that call used another stream, and records its own end.  Skipped under
+// stream capture (a captured graph is ordered by the stream it is launched on).
+struct StreamUse {
+  ttagg_ctx* ctx;
+  cudaStream_t st;
+  bool active = false;
+  int enter(ttagg_ctx* c, cudaStream_t s) {
+    ctx = c;
+    st = s;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return TTAGG_OK;
+    if (!ctx->ev_last) CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_last, cudaEventDisableTiming));
+    if (ctx->last_valid && ctx->last_stream != s) CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev_last, 0));
+    active = true;
+    return TTAGG_OK;
+  }
+  ~StreamUse() {
+    if (active && cudaEventRecord(ctx->ev_last, st) == cudaSuccess) {
+      ctx->last_stream = st;
+      ctx->last_valid = true;
+    }
+  }
+};
+
 // Run all orders: gains into pbuf, loss coefficients; fill the combine descriptor.
 // Several orders: the main stream runs the pass A of every cheaper order, then
 // pass A and pass B/C of the costliest order; the cheaper orders' pass B/C run
@@ -1737,7 +1815,9 @@ int ttagg_ctx_destroy(ttagg_ctx* ctx) {
   for (cudaEvent_t e : {ctx->ev_a, ctx->ev_fill})
     if (e) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_last) cudaEventDestroy(ctx->ev_last);
   cudaFree(ctx->pbuf);
+  if (ctx->pin) cudaFreeHost(ctx->pin);
   cudaFree(ctx->vec);
   cudaFree(ctx->diagp);
   cudaFree(ctx->diag);
@@ -1750,6 +1830,18 @@ int ttagg_ctx_destroy(ttagg_ctx* ctx) {
   delete ctx;
   return TTAGG_OK;
 }
+
+// upload scratch, freed on every return path
+struct Scratch {
+  double* src = nullptr;
+  int* sel = nullptr;
+  int* map = nullptr;
+  ~Scratch() {
+    cudaFree(src);
+    cudaFree(sel);
+    cudaFree(map);
+  }
+};
 
 // Frees a kernel's device buffers (cudaFree(nullptr) is a no-op) and the
 // handle; upload failures release a partially built kernel through
@@ -1827,11 +1919,12 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
   CUDA_TRY(cudaMalloc(&k->Xt, std::max<size_t>(1, k->R) * colbytes));
   std::vector<int> tails;
   if (k->R > 0) {
-    double* dsrc = nullptr;
-    int *dsel = nullptr, *dmap = nullptr;
-    CUDA_TRY(cudaMalloc(&dsrc, (size_t)n_classes * rank * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&dsel, sel.size() * sizeof(int)));
-    CUDA_TRY(cudaMalloc(&dmap, sel.size() * sizeof(int)));
+    Scratch sc;
+    CUDA_TRY(cudaMalloc(&sc.src, (size_t)n_classes * rank * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&sc.sel, sel.size() * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&sc.map, sel.size() * sizeof(int)));
+    double* dsrc = sc.src;
+    int *dsel = sc.sel, *dmap = sc.map;
     CUDA_TRY(cudaMemcpy(dsel, sel.data(), sel.size() * sizeof(int), cudaMemcpyHostToDevice));
     for (int m = 0; m < d; ++m) {
       if (!factors[m]) return fail(TTAGG_ERR_ARG, "null factor");
@@ -1851,9 +1944,6 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
       }
     }
     CUDA_TRY(cudaDeviceSynchronize());
-    cudaFree(dsrc);
-    cudaFree(dsel);
-    cudaFree(dmap);
     for (int j = 0; j < k->R; ++j) tails.push_back(j);  // rows of Xt
   }
   TRY(finish_upload(ctx, k, tails));
@@ -1967,13 +2057,14 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
   CUDA_TRY(cudaMalloc(&k->X, std::max<size_t>(2, k->C_pad) * colbytes));
   CUDA_TRY(cudaMemset(k->X, 0, std::max<size_t>(2, k->C_pad) * colbytes));
   CUDA_TRY(cudaMalloc(&k->Xt, std::max<size_t>(1, k->ranks[d - 1]) * colbytes));
-  double* dsrc = nullptr;
-  int *dsel = nullptr, *dmap = nullptr;
+  Scratch sc;
   size_t maxcore = 0;
   for (int l = 0; l < d; ++l) maxcore = std::max(maxcore, (size_t)k->ranks[l] * n_classes * k->ranks[l + 1]);
-  CUDA_TRY(cudaMalloc(&dsrc, maxcore * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&dsel, 64 * 64 * sizeof(int)));
-  CUDA_TRY(cudaMalloc(&dmap, 64 * 64 * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&sc.src, maxcore * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&sc.sel, 64 * 64 * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&sc.map, 64 * 64 * sizeof(int)));
+  double* dsrc = sc.src;
+  int *dsel = sc.sel, *dmap = sc.map;
   for (int l = 0; l < d; ++l) {
     const int rp_n = k->ranks[l], rn_n = k->ranks[l + 1];
     CUDA_TRY(cudaMemcpy(dsrc, cores[l], (size_t)rp_n * n_classes * rn_n * sizeof(double), cudaMemcpyHostToDevice));
@@ -2006,9 +2097,6 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
       CUDA_TRY(cudaDeviceSynchronize());
     }
   }
-  cudaFree(dsrc);
-  cudaFree(dsel);
-  cudaFree(dmap);
   std::vector<int> tails;
   for (int rp = 0; rp < k->ranks[d - 1]; ++rp) tails.push_back(rp);  // rows of Xt
   TRY(finish_upload(ctx, k, tails));
@@ -2087,6 +2175,8 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   Geom g;
   TRY(check_set(kernels, n_kernels, &g));
   cudaStream_t st = (cudaStream_t)stream;
+  StreamUse use;
+  TRY(use.enter(ctx, st));
   bool wantP = flags & TTAGG_WANT_P, wantQ = flags & TTAGG_WANT_Q;
   if (!wantP && !wantQ) wantP = wantQ = true;
   const bool host = flags & TTAGG_HOST_PTRS;
@@ -2101,9 +2191,26 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   double* v_s = v_q + Na;
   const double* nsrc = n;
   int* dflag = reinterpret_cast<int*>(ctx->book + 6);
+  // host-pointer path: pageable buffers go through the context's page-locked
+  // staging area ([n][p][q][s], copied by a few host threads); pinned ones
+  // are transferred directly
+  double* out_host[3] = {p, q, s};
+  double* out_stage[3] = {nullptr, nullptr, nullptr};
   if (host) {
+    const bool in_pinned = is_pinned(n);
+    bool need_stage = !in_pinned;
+    for (double* o : out_host) need_stage |= (o && !is_pinned(o));
+    if (need_stage) TRY(ensure_pinned(ctx, 4 * Na * sizeof(double)));
     CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), st));
-    CUDA_TRY(cudaMemcpyAsync(v_nat, n, nb, cudaMemcpyHostToDevice, st));
+    const double* src = n;
+    if (!in_pinned) {
+      CUDA_TRY(cudaStreamSynchronize(st));  // the staging area may still feed an earlier copy
+      par_copy(ctx->pin, n, nb);
+      src = ctx->pin;
+    }
+    for (int i = 0; i < 3; ++i)
+      if (out_host[i] && !is_pinned(out_host[i])) out_stage[i] = ctx->pin + (size_t)(i + 1) * Na;
+    CUDA_TRY(cudaMemcpyAsync(v_nat, src, nb, cudaMemcpyHostToDevice, st));
     nsrc = v_nat;
   }
   TRY(launch_permute(nsrc, v_perm, g, 0, st, host ? dflag : nullptr));
@@ -2124,11 +2231,14 @@ int ttagg_rhs(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   if (host) {
     int hflag = 0;
     CUDA_TRY(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    if (p) CUDA_TRY(cudaMemcpyAsync(p, v_p, nb, cudaMemcpyDeviceToHost, st));
-    if (q) CUDA_TRY(cudaMemcpyAsync(q, v_q, nb, cudaMemcpyDeviceToHost, st));
-    if (s) CUDA_TRY(cudaMemcpyAsync(s, v_s, nb, cudaMemcpyDeviceToHost, st));
+    const double* dev_out[3] = {v_p, v_q, v_s};
+    for (int i = 0; i < 3; ++i)
+      if (out_host[i])
+        CUDA_TRY(cudaMemcpyAsync(out_stage[i] ? out_stage[i] : out_host[i], dev_out[i], nb, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if (hflag) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
+    for (int i = 0; i < 3; ++i)
+      if (out_stage[i]) par_copy(out_host[i], out_stage[i], nb);
   }
   return TTAGG_OK;
 }
@@ -2141,6 +2251,8 @@ int ttagg_rhs_perm(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_ker
   Geom g;
   TRY(check_set(kernels, n_kernels, &g));
   cudaStream_t st = (cudaStream_t)stream;
+  StreamUse use;
+  TRY(use.enter(ctx, st));
   CombineArgs A{};
   TRY(run_orders(ctx, kernels, n_kernels, n_perm, k_perm, alpha, true, true, &A, st));
   A.out_perm = s_perm;
@@ -2168,6 +2280,8 @@ int ttagg_stage(ttagg_ctx* ctx, int64_t n_classes, const double* base, const dou
   Geom g;
   TRY(make_geom(n_classes, &g));
   cudaStream_t st = (cudaStream_t)stream;
+  StreamUse use;
+  TRY(use.enter(ctx, st));
   const int nb = (int)((g.Np + 255) / 256);
   double* dp = nullptr;
   if (diag) {
@@ -2186,7 +2300,6 @@ int ttagg_stage(ttagg_ctx* ctx, int64_t n_classes, const double* base, const dou
 int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels, double* n_inout, double t0,
               double dt, int64_t steps, int64_t record_every, double* records, int64_t* fail_step,
               int64_t* neg_step, int flags, void* stream) {
-  (void)t0;
   if (!ctx || !n_inout || !records || !fail_step || !neg_step) return fail(TTAGG_ERR_ARG, "null argument");
   if (!(dt > 0)) return fail(TTAGG_ERR_ARG, "dt must be positive");
   if (steps < 1 || record_every < 1) return fail(TTAGG_ERR_ARG, "steps and record_every must be >= 1");
@@ -2197,6 +2310,31 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   cudaStream_t st = (cudaStream_t)stream;
   const bool host = flags & TTAGG_HOST_PTRS;
   const int64_t nrows = steps / record_every + 1;
+  // graphs and the stream this call may create are released on every path
+  struct Owned {
+    cudaGraphExec_t ge[2] = {nullptr, nullptr};
+    cudaStream_t own = nullptr;
+    ~Owned() {
+      for (auto& e : ge)
+        if (e) cudaGraphExecDestroy(e);
+      if (own) {
+        cudaStreamSynchronize(own);
+        cudaStreamDestroy(own);
+      }
+    }
+  } owned;
+  const bool use_graph = !ctx->prof;
+  cudaStream_t cap = st;
+  if (use_graph && st == nullptr) {
+    // the legacy stream cannot be captured: run on a stream of our own, after
+    // everything already queued on the device
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaStreamCreateWithFlags(&owned.own, cudaStreamNonBlocking));
+    cap = owned.own;
+  }
+  st = cap;
+  StreamUse use;
+  TRY(use.enter(ctx, st));
   // vec layout: [nat N][A Np][B Np][C Np][rec nrows*4]
   const size_t nb = (size_t)g.N * sizeof(double);
   const int64_t Na = (g.N + 31) & ~(int64_t)31;  // 256-byte aligned sub-buffers
@@ -2213,14 +2351,18 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   double* dmid = ctx->diag;
   double* dnew = ctx->diag + DIAGW;
   double* d0 = ctx->diag + 2 * DIAGW;
-  if (host) {
-    for (int64_t i = 0; i < g.N; ++i)
-      if (!std::isfinite(n_inout[i])) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
-    CUDA_TRY(cudaMemcpyAsync(v_nat, n_inout, nb, cudaMemcpyHostToDevice, st));
-  } else {
-    CUDA_TRY(cudaMemcpyAsync(v_nat, n_inout, nb, cudaMemcpyDeviceToDevice, st));
+  // the initial state's finiteness (ConcentrationState, rhs.py:71-72) is
+  // checked on the device while it is permuted
+  int* dflag = reinterpret_cast<int*>(ctx->book + 6);
+  CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), st));
+  CUDA_TRY(cudaMemcpyAsync(v_nat, n_inout, nb, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+  TRY(launch_permute(v_nat, vA, g, 0, st, dflag));
+  {
+    int hflag = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (hflag) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
   }
-  TRY(launch_permute(v_nat, vA, g, 0, st));
   // initial record
   stage_kernel<<<nblk, 256, 0, st>>>(vA, vA, 0.0, nullptr, g.N, g.N1, g.N2, dpn);
   diag_finalize_kernel<<<1, 256, 0, st>>>(dpn, nblk, d0);
@@ -2252,41 +2394,34 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
     CUDA_TRY(cudaGetLastError());
     return TTAGG_OK;
   };
-  // capture one step for each buffer parity into CUDA graphs
-  const bool use_graph = !ctx->prof;
-  cudaGraphExec_t ge[2] = {nullptr, nullptr};
-  cudaStream_t cap = st;
-  bool own_stream = false;
-  if (use_graph && st == nullptr) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    own_stream = true;
-    CUDA_TRY(cudaDeviceSynchronize());
-  }
   int64_t host_book[4] = {0, 0, 0, 0};
-  int rc = TTAGG_OK;
   if (use_graph) {
-    // make sure workspaces exist before capture (allocation is not capturable)
-    st = cap;
-    TRY(step_once(cur, mid, nxt));  // step 1 runs eagerly
+    // capture one step for each buffer parity into CUDA graphs; step 1 runs
+    // eagerly (workspaces are allocated before capture, which cannot allocate)
+    TRY(step_once(cur, mid, nxt));
     std::swap(cur, nxt);
     for (int par = 0; par < 2 && steps > 1; ++par) {
       double* c0 = par == 0 ? cur : nxt;
       double* c1 = par == 0 ? nxt : cur;
-      cudaGraph_t gr;
+      cudaGraph_t gr = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-      rc = step_once(c0, mid, c1);
-      cudaError_t ec = cudaStreamEndCapture(cap, &gr);
-      if (rc) return rc;
+      const int rc = step_once(c0, mid, c1);
+      const cudaError_t ec = cudaStreamEndCapture(cap, &gr);
+      if (rc) {
+        if (gr) cudaGraphDestroy(gr);
+        return rc;
+      }
       if (ec != cudaSuccess) return fail(TTAGG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
-      CUDA_TRY(cudaGraphInstantiate(&ge[par], gr, 0));
+      const cudaError_t ei = cudaGraphInstantiate(&owned.ge[par], gr, 0);
       cudaGraphDestroy(gr);
+      if (ei != cudaSuccess) return fail(TTAGG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
     }
     int64_t done = 1;
     int par = 0;
     while (done < steps) {
       const int64_t chunk = std::min<int64_t>(steps - done, 64);
       for (int64_t i = 0; i < chunk; ++i) {
-        CUDA_TRY(cudaGraphLaunch(ge[par], cap));
+        CUDA_TRY(cudaGraphLaunch(owned.ge[par], cap));
         par ^= 1;
       }
       done += chunk;
@@ -2295,8 +2430,6 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
       if (host_book[1] != 0) break;
     }
     if (par == 1) std::swap(cur, nxt);  // final state location
-    for (auto& e : ge)
-      if (e) cudaGraphExecDestroy(e);
   } else {
     for (int64_t s = 1; s <= steps; ++s) {
       TRY(step_once(cur, mid, nxt));
@@ -2310,20 +2443,25 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
   }
   CUDA_TRY(cudaMemcpyAsync(host_book, ctx->book, sizeof(host_book), cudaMemcpyDeviceToHost, cap));
   TRY(launch_permute(cur, v_nat, g, 1, cap));
-  // records: device rows (M0, M1, M2, min) -> (t, M0, M1, M2, min) with t filled by the caller
+  // records: device rows (M0, M1, M2, min) -> (t, M0, M1, M2, min)
   std::vector<double> hrec((size_t)nrows * 4);
   CUDA_TRY(cudaMemcpyAsync(hrec.data(), rec, hrec.size() * sizeof(double), cudaMemcpyDeviceToHost, cap));
-  if (host) {
-    CUDA_TRY(cudaMemcpyAsync(n_inout, v_nat, nb, cudaMemcpyDeviceToHost, cap));
-  } else {
-    CUDA_TRY(cudaMemcpyAsync(n_inout, v_nat, nb, cudaMemcpyDeviceToDevice, cap));
-  }
+  CUDA_TRY(cudaMemcpyAsync(n_inout, v_nat, nb, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, cap));
   CUDA_TRY(cudaStreamSynchronize(cap));
-  if (own_stream) cudaStreamDestroy(cap);
-  const int64_t rows = host_book[3];
+  const int64_t rows = std::min<int64_t>(host_book[3], nrows);
   std::vector<double> out((size_t)nrows * 5, 0.0);
-  for (int64_t r = 0; r < rows && r < nrows; ++r)
-    for (int c = 0; c < 4; ++c) out[r * 5 + 1 + c] = hrec[r * 4 + c];
+  // times as the reference accumulates them (state.t + dt per step,
+  // integrator.py:179, 207): row r holds step r * record_every
+  double t = t0;
+  int64_t row = 0;
+  for (int64_t step = 0; row < rows; ++step) {
+    if (step > 0) t = t + dt;
+    if (step % record_every == 0) {
+      out[row * 5] = t;
+      for (int c = 0; c < 4; ++c) out[row * 5 + 1 + c] = hrec[row * 4 + c];
+      ++row;
+    }
+  }
   if (host) {
     std::memcpy(records, out.data(), out.size() * sizeof(double));
   } else {

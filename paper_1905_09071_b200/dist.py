@@ -69,7 +69,7 @@ class CudaEngine:
                 self.dks.append(self.ctx.upload_cp(factors_by_order[d], rank_subset=sub))
         for d in sorted(tt_cores or {}):
             self.dks.append(self.ctx.upload_tt(tt_cores[d]))
-        self.diag = torch.zeros(8, dtype=torch.float64, device=self.device)
+        self.diag = torch.zeros((2, 8), dtype=torch.float64, device=self.device)
 
     def vector(self):
         return self.torch.zeros(self.Np, dtype=self.torch.float64, device=self.device)
@@ -96,12 +96,15 @@ class CudaEngine:
         else:
             out.zero_()
 
-    def stage(self, base, s, a, out):
-        """out = base + a s; returns (nonfinite, min, max|.|, M0, M1, M2)."""
+    def stage(self, base, s, a, out, slot=0):
+        """out = base + a s; diagnostics (nonfinite, min, max|.|, M0, M1, M2)
+        stay on the device in `slot` until :meth:`diags` reads them."""
         self.ctx.stage(self.n_classes, base.data_ptr(), s.data_ptr(), a,
-                       None if out is None else out.data_ptr(), self.diag.data_ptr(), self._stream())
-        d = self.diag.cpu().numpy()
-        return d[:6]
+                       None if out is None else out.data_ptr(), self.diag[slot].data_ptr(), self._stream())
+
+    def diags(self) -> np.ndarray:
+        """Both diagnostic slots in one device-to-host read: (2, 6)."""
+        return self.diag.cpu().numpy()[:, :6]
 
 
 @dataclass
@@ -143,15 +146,17 @@ class DistRHS:
         mid = e.vector()
         nxt = e.vector()
         zero = e.vector()
-        d0 = e.stage(n, zero, 0.0, None)  # diagnostics of the initial state
+        e.stage(n, zero, 0.0, None, 0)
+        d0 = e.diags()[0]  # diagnostics of the initial state
         res = DistRK2Result(n=np.asarray(n0))
         res.rows.append((float(t0), float(d0[3]), float(d0[4]), float(d0[5]), float(d0[1])))
         t = float(t0)
         for step in range(1, steps + 1):
             self.rhs(n, out=s)
-            dm = e.stage(n, s, 0.5 * dt, mid)
+            e.stage(n, s, 0.5 * dt, mid, 0)
             self.rhs(mid, out=s)
-            dn = e.stage(n, s, dt, nxt)
+            e.stage(n, s, dt, nxt, 1)
+            dm, dn = e.diags()  # one host sync per step
             if dm[0] != 0.0 or dn[0] != 0.0:
                 res.fail_step = step
                 break

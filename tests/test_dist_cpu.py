@@ -27,6 +27,7 @@ class OracleEngine:
         self.shard = shard
         self.n_classes = n_classes
         self.tt = tt_cores or {}
+        self._diag = np.zeros((2, 6))
 
     def vector(self):
         return torch.zeros(self.n_classes, dtype=torch.float64)
@@ -50,13 +51,16 @@ class OracleEngine:
             acc += orc.tt_loss(self.tt[d], x)
         out.copy_(torch.from_numpy(acc))
 
-    def stage(self, base, s, a, out):
+    def stage(self, base, s, a, out, slot=0):
         v = (base + a * s).numpy()
         k = np.arange(1, v.size + 1, dtype=np.float64)
         if out is not None:
             out.copy_(torch.from_numpy(v))
-        return np.array([0.0 if np.all(np.isfinite(v)) else 1.0, v.min(), np.abs(v).max(),
-                         v.sum(), k @ v, (k * k) @ v])
+        self._diag[slot] = np.array([0.0 if np.all(np.isfinite(v)) else 1.0, v.min(), np.abs(v).max(),
+                                     v.sum(), k @ v, (k * k) @ v])
+
+    def diags(self):
+        return self._diag.copy()
 
 
 def _free_port():

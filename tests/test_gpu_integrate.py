@@ -277,3 +277,26 @@ def test_c4_full_size_vs_reference(golden):
         assert abs(sums[i] - c["n2_sums"][i]) <= TRAJ_TOL * abs(c["n2_sums"][i])
     rows = np.array(series.rows())
     assert np.allclose(rows[:, :3], c["n2_rows"][:, :3], rtol=TRAJ_TOL, atol=0.0)
+
+
+def test_config_kernels_match_reference_cli(golden):
+    """integrate(config) with kernels=None builds the reference's default
+    kernels from the config's specs in-repo (construct.kernel_set_from_config,
+    config.py:231-242: Brownian -> exact TT) and matches the reference's own
+    `ttagg simulate` run (moments.csv rows and the final snapshot n_40.csv,
+    oracle/make_golden.py cli)."""
+    import json
+    from types import SimpleNamespace
+
+    ref = golden("cli.npz")
+    c = json.loads(str(ref["config"]))
+    specs = {int(d): SimpleNamespace(exponents=tuple(k["mu"]), dimension=len(k["mu"]))
+             for d, k in c["kernels"].items()}
+    cfg = SimpleNamespace(n_classes=c["N"], kernel_specs=specs,
+                          initial=g.InitialCondition.monodisperse(c["initial"]["c0"]),
+                          time=g.TimeGrid(c["time"]["t0"], c["time"]["dt"], c["time"]["steps"]),
+                          record_every=c["record_every"])
+    final, series = g.integrate(cfg)
+    assert rel_inf(final.n, ref["n_final"]) <= TRAJ_TOL
+    assert_rows(series.rows(), ref["rows"], TRAJ_TOL)
+    assert final.t == ref["rows"][-1, 0]

@@ -187,6 +187,28 @@ def test_c5_full_size_vs_reference(golden):
     assert rel_inf(r2.s, r.s) <= 1e-14
 
 
+def test_c5_full_vectors_vs_oracle_on_the_box():
+    """Full-vector (not sampled) p, q and s at N = 2^20, D = 5 against the
+    oracle evaluated here on the host cores: every rank term of every order
+    through the reference algorithm (pow2 transform length, rhs.py:345-414),
+    about 25 s on 16 threads."""
+    import os
+
+    cfg = CONFIGS["C5"]
+    N = cfg.n_classes
+    n = initial_state("c5", N)
+    fs = {d: permutation_power_cp(cfg.exponents[:d], N) for d in cfg.orders}
+    r = g.rhs_total(g.KernelSet({d: g.CPKernel(f) for d, f in fs.items()}), st(n))
+    w = os.cpu_count() or 1
+    p = q = 0.0
+    for d in cfg.orders:
+        p = p + orc.cp_gain(fs[d], n, workers=w, rank_chunk=max(1, 128 // d))
+        q = q + orc.cp_loss(fs[d], n)
+    assert rel_inf(r.p, p) <= TOL
+    assert rel_inf(r.q, q) <= TOL
+    assert rel_inf(r.s, p + q) <= TOL
+
+
 def test_c5_full_size_closed_form_every_order():
     """FFT-length-independent property at full size: the permutation-power
     gain equals the collapsed d-fold convolution."""

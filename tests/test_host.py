@@ -216,3 +216,104 @@ def test_dense_kernel_container_and_budget():
         g.rhs_dense_P(g.DenseKernel(np.zeros((8193, 8193))), g.ConcentrationState(np.ones(8193)))
     with pytest.raises(g.KernelError, match="budget"):
         g.rhs_total(g.KernelSet({2: g.DenseKernel(np.zeros((8193, 8193)))}), g.ConcentrationState(np.ones(8193)))
+
+
+def _reference():
+    import os
+    import sys
+
+    if os.path.isdir("/root/reference/pkg/src") and "/root/reference/pkg/src" not in sys.path:
+        sys.dont_write_bytecode = True
+        sys.path.append("/root/reference/pkg/src")
+    return pytest.importorskip("ttagg")
+
+
+def test_brownian_tt_matches_reference_builder():
+    """construct.brownian_tt restates build_brownian_tt (kernels.py:332-363):
+    the same cores, bit for bit, so integrate(config) needs no reference."""
+    ttagg = _reference()
+    from paper_1905_09071_b200.construct import brownian_tt
+
+    for mus in ((0.3, -0.3), (0.2, -0.1, -0.1), (0.1, -0.1, 0.05, -0.05, 0.0)):
+        ref = ttagg.build_brownian_tt(ttagg.BrownianSpec(mus), 257).cores
+        got = brownian_tt(mus, 257)
+        assert len(got) == len(ref)
+        for a, b in zip(got, ref):
+            assert a.shape == b.shape
+            np.testing.assert_array_equal(a, b)
+
+
+def test_kernel_set_from_config_matches_reference(tmp_path):
+    """Brownian -> exact TT, constant -> rank-1 TT, table -> dense
+    (config.py:231-242), from the reference's own SimulationConfig."""
+    ttagg = _reference()
+    from ttagg.config import build_kernel_set, config_from_dict
+
+    from paper_1905_09071_b200.construct import kernel_set_from_config
+
+    table = tmp_path / "k2.bin"
+    rng = np.random.default_rng(5)
+    vals = rng.random((16, 16))
+    vals = vals + vals.T
+    vals.astype("<f8").tofile(table)
+    cfg = config_from_dict({"N": 16, "D": 4, "time": {"dt": 0.01, "steps": 1},
+                            "kernels": {"2": {"type": "table", "table_path": str(table)},
+                                        "3": {"type": "constant", "c": 2.5},
+                                        "4": {"type": "brownian", "mu": [0.1, -0.1, 0.2, 0.0]}}})
+    ref = build_kernel_set(cfg)
+    got = kernel_set_from_config(cfg)
+    np.testing.assert_array_equal(got[2].values, ref[2].values)
+    for d in (3, 4):
+        for a, b in zip(got[d].cores, ref[d].cores):
+            np.testing.assert_array_equal(a, b)
+
+
+def _oracle_total(kernels, state, plan=None, *, breakdown=False):
+    """CPU stand-in for the GPU rhs_total (host-logic test double only)."""
+    from types import SimpleNamespace
+
+    from oracle import rhs_oracle as orc
+
+    ks = {d: {"kind": "tt", "arrays": kernels[d].cores} for d in kernels.orders}
+    p, q, s = orc.rhs_total(ks, state.n)
+    return SimpleNamespace(p=p, q=q, s=s, by_order=None)
+
+
+def test_install_routes_reference_cli_through_package_integrate(tmp_path, golden, monkeypatch):
+    """After install(), the reference's own `ttagg simulate` (cli.py:80-110,
+    which bound `integrate` at import, cli.py:21) runs the package's
+    integrate: kernels built from the config's specs in-repo, records and
+    snapshots through the reference's types and writers.  The device RHS is
+    replaced by the oracle here (no GPU on this host); the GPU twin is
+    tests/test_gpu_integrate.py::test_config_kernels_match_reference_cli."""
+    import json
+
+    ttagg = _reference()
+    import ttagg.cli as tc
+    import ttagg.integrator as ti
+
+    import paper_1905_09071_b200.integrator as gi
+
+    monkeypatch.setattr(gi, "rhs_total", _oracle_total)
+    ref = golden("cli.npz")
+    cfg = json.loads(str(ref["config"]))
+    path = tmp_path / "run.json"
+    path.write_text(json.dumps(cfg))
+    undo = g.install(ttagg)
+    try:
+        assert tc.integrate is ti.integrate and ti.integrate is not gi.integrate
+        assert tc.main(["simulate", "--config", str(path), "--output", str(tmp_path / "out")]) == 0
+        rows = np.loadtxt(tmp_path / "out" / "moments.csv", delimiter=",", skiprows=1)
+        snap = np.loadtxt(tmp_path / "out" / "n_40.csv", delimiter=",", skiprows=1)[:, 1]
+        assert rows.shape == ref["rows"].shape
+        from conftest import assert_rows
+
+        assert_rows(rows, ref["rows"], 1e-9)  # FFT roundoff differs from the reference's plan
+        np.testing.assert_allclose(snap, ref["n_final"], rtol=0, atol=1e-10 * np.abs(ref["n_final"]).max())
+        # a diverging run maps to the CLI's numerical-failure exit code (cli.py:236-238)
+        cfg_bad = dict(cfg, time={"t0": 0.0, "dt": 1e6, "steps": 3})
+        path.write_text(json.dumps(cfg_bad))
+        assert tc.main(["simulate", "--config", str(path), "--output", str(tmp_path / "bad")]) == 2
+    finally:
+        undo()
+    assert tc.integrate is not ti.rhs_total and ti.integrate.__module__ == "ttagg.integrator"

@@ -18,7 +18,6 @@ ctx = _lib.get_context()
 dks = [ctx.device_kernel(ks[d]) for d in ks.orders]
 print("ConcentrationState(n0)      %.2f ms" % tm(lambda: g.ConcentrationState(n0)))
 print("np.isfinite(n0).all()       %.2f ms" % tm(lambda: np.isfinite(n0).all()))
-print("ctx._stage_input            %.2f ms" % tm(lambda: ctx._stage_input(n0)))
 print("ctx._pinned(N, 3)           %.2f ms" % tm(lambda: ctx._pinned(N, 3)))
 print("ctx.rhs_host(dks, n)        %.2f ms" % tm(lambda: ctx.rhs_host(dks, n0)))
 print("g.rhs_total(ks, st)         %.2f ms" % tm(lambda: g.rhs_total(ks, st)))
