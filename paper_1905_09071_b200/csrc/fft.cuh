@@ -214,7 +214,8 @@ __device__ __forceinline__ void twiddle16(cplx* x, cplx w1, cplx w4) {
 
 // One stage.  Registers: element t + T*r in v[r] on entry (read pattern).
 template <int M, int R, int NS, bool LAST>
-__device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
+                                          const double2* stw = nullptr) {
   constexpr int E = fft_e(M);
   constexpr int T = fft_t(M);
   constexpr int G = E / R;  // butterflies per thread
@@ -232,7 +233,8 @@ __device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* s
 #define TTAGG_TW_MODE 0
 #endif
       if constexpr (R == 16 && TTAGG_TW_MODE == 0) {
-        twiddle16(x, ld_c(tw + e), ld_c(tw + 4 * e));
+        if (stw) twiddle16(x, lds_c(stw + qm), lds_c(stw + NS + qm));
+        else twiddle16(x, ld_c(tw + e), ld_c(tw + 4 * e));
       } else if constexpr (R == 16 && TTAGG_TW_MODE == 2) {
         // w1..w3 and w4, w8, w12 loaded; 9 products
         const cplx w1 = ld_c(tw + e), w2 = ld_c(tw + 2 * e), w3 = ld_c(tw + 3 * e);
@@ -270,9 +272,12 @@ __device__ __forceinline__ void fft_load_regs(cplx (&v)[fft_e(M)], int t, const 
 // Forward FFT of length M (no normalisation).  All threads of the CTA must
 // call it (it contains __syncthreads when M > 16); `sm` is this transform's
 // private buffer of fft_smem_elems(M) slots.
+template <int M>
+__host__ __device__ constexpr int fft_stage_ns(int which);
+
 template <int M, class Sync = CtaSync>
 __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
-                                        const Sync& sync = Sync()) {
+                                        const Sync& sync = Sync(), const double2* stw = nullptr) {
   if constexpr (M <= 16) {
     DFT<M>::run(v);
     // DFT<R> leaves natural order, and with T == 1 register r == frequency r
@@ -292,22 +297,22 @@ __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm,
     if constexpr (a == 1) {
       fft_stage<M, 16, NS1, true>(v, t, sm, tw);
     } else if constexpr (a == 2) {
-      fft_stage<M, 16, NS1, false>(v, t, sm, tw);
+      fft_stage<M, 16, NS1, false>(v, t, sm, tw, stw);
       sync();
       fft_load_regs<M>(v, t, sm);
       sync();
-      fft_stage<M, 16, NS1 * 16, true>(v, t, sm, tw);
+      fft_stage<M, 16, NS1 * 16, true>(v, t, sm, tw, stw ? stw + 2 * fft_stage_ns<M>(0) : nullptr);
     } else {
       static_assert(a == 3, "M <= 4096");
       fft_stage<M, 16, NS1, false>(v, t, sm, tw);
       sync();
       fft_load_regs<M>(v, t, sm);
       sync();
-      fft_stage<M, 16, NS1 * 16, false>(v, t, sm, tw);
+      fft_stage<M, 16, NS1 * 16, false>(v, t, sm, tw, stw);
       sync();
       fft_load_regs<M>(v, t, sm);
       sync();
-      fft_stage<M, 16, NS1 * 256, true>(v, t, sm, tw);
+      fft_stage<M, 16, NS1 * 256, true>(v, t, sm, tw, stw ? stw + 2 * fft_stage_ns<M>(0) : nullptr);
     }
     (void)ns_done;
   }
@@ -349,6 +354,105 @@ __device__ __forceinline__ void fft_fwd2(cplx (&v1)[fft_e(M)], cplx (&v2)[fft_e(
     xchg();
     fft_stage<M, 16, NS1 * 256, true>(v1, t, sm1, tw);
     fft_stage<M, 16, NS1 * 256, true>(v2, t, sm2, tw);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Half-footprint exchanges: the same transform with every exchange done in
+// two rounds (real parts, then imaginary parts) through a buffer of
+// fft_smem_elems(M) doubles — half the shared memory of fft_fwd, two more
+// barriers per exchange, no extra registers (a value's real and imaginary
+// halves live in separate registers, so the new real parts can land while
+// the old imaginary parts still wait to be written).
+// ---------------------------------------------------------------------------
+template <int M, int R, int NS, class Sync>
+__device__ __forceinline__ void fft_stage_split(cplx (&v)[fft_e(M)], int t, double* sm, const double2* __restrict__ tw,
+                                                const Sync& sync, const double2* stw = nullptr) {
+  constexpr int E = fft_e(M);
+  constexpr int T = fft_t(M);
+  constexpr int G = E / R;
+  int dst[E];
+#pragma unroll
+  for (int u = 0; u < G; ++u) {
+    const int q = t + T * u;
+    cplx x[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) x[i] = v[u + i * G];
+    if constexpr (NS > 1) {
+      const int qm = q & (NS - 1);
+      const int e = qm * (TW_BASE / (NS * R));
+      if constexpr (R == 16) {
+        if (stw) twiddle16(x, lds_c(stw + qm), lds_c(stw + NS + qm));
+        else twiddle16(x, ld_c(tw + e), ld_c(tw + 4 * e));
+      } else {
+#pragma unroll
+        for (int i = 1; i < R; ++i) x[i] = cmul(x[i], ld_c(tw + i * e));
+      }
+    }
+    DFT<R>::run(x);
+    const int base = (q / NS) * NS * R + (q & (NS - 1));
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      v[u + i * G] = x[i];
+      dst[u + i * G] = pad16(base + i * NS);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < E; ++r) sm[dst[r]] = v[r].x;
+  sync();
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r].x = sm[pad16(t + T * r)];
+  sync();
+#pragma unroll
+  for (int r = 0; r < E; ++r) sm[dst[r]] = v[r].y;
+  sync();
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r].y = sm[pad16(t + T * r)];
+  sync();
+}
+
+// Stage-twiddle table for the twiddled radix-16 stages of a length-M
+// transform (shared memory, filled once per CTA by fft_stage_table): for each
+// such stage with NS sub-transforms, w1[NS] then w4[NS] (w = W_{16 NS}^qm).
+// Its reads are unit-stride across the warp, where the W_4096 table gathers
+// touch up to 16 lines per warp load.
+template <int M>
+__host__ __device__ constexpr int fft_stage_ns(int which) {  // NS of the two twiddled radix-16 stages
+  return M >= 4096 ? (which ? 256 : 16) : (which ? 16 * fft_first_radix(M) : fft_first_radix(M));
+}
+template <int M>
+__host__ __device__ constexpr int fft_stage_table_elems() {
+  return 2 * (fft_stage_ns<M>(0) + fft_stage_ns<M>(1));
+}
+template <int M>
+__device__ __forceinline__ void fft_stage_table(double2* stw, const double2* __restrict__ tw, int t, int nthreads) {
+  constexpr int NSa = fft_stage_ns<M>(0), NSb = fft_stage_ns<M>(1);
+  for (int i = t; i < 2 * (NSa + NSb); i += nthreads) {
+    const bool second = i >= 2 * NSa;
+    const int NS = second ? NSb : NSa;
+    const int k = second ? i - 2 * NSa : i;
+    const int qm = k % NS, pw = k < NS ? 1 : 4;
+    stw[i] = tw[pw * qm * (TW_BASE / (NS * 16))];
+  }
+}
+
+template <int M, class Sync = CtaSync>
+__device__ __forceinline__ void fft_fwd_split(cplx (&v)[fft_e(M)], int t, double* sm, const double2* __restrict__ tw,
+                                              const Sync& sync = Sync(), const double2* stw = nullptr) {
+  static_assert(M >= 256 && M <= 4096, "block transforms");
+  constexpr int b = fft_first_radix(M);
+  constexpr int a = (ilog2c(M) - ilog2c(b)) / 4;
+  constexpr int off = 2 * fft_stage_ns<M>(0);
+  if constexpr (b > 1) fft_stage_split<M, b, 1>(v, t, sm, tw, sync);
+  constexpr int NS1 = b;
+  if constexpr (a == 2) {
+    fft_stage_split<M, 16, NS1>(v, t, sm, tw, sync, stw);
+    fft_stage<M, 16, NS1 * 16, true>(v, t, nullptr, tw, stw ? stw + off : nullptr);
+  } else {
+    static_assert(a == 3, "M <= 4096");
+    fft_stage_split<M, 16, NS1>(v, t, sm, tw, sync);
+    fft_stage_split<M, 16, NS1 * 16>(v, t, sm, tw, sync, stw);
+    fft_stage<M, 16, NS1 * 256, true>(v, t, nullptr, tw, stw ? stw + off : nullptr);
   }
 }
 

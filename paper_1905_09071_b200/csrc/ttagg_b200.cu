@@ -30,6 +30,7 @@
 // "perm" layout (element o = n1*N2 + n2 at n2*N1 + n1), so pass A reads each
 // column with unit stride; factor columns / TT fibers are stored once, at
 // upload, in that layout.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -444,6 +445,170 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_big_kernel(const PassAArgs
   }
 }
 
+// ---- bulk-copy (TMA) and mbarrier helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on mbarrier m
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TTAGG_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TTAGG_WAIT_%=;\n}" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+
+// Pass A, TMA-fed (N1 >= 1024): persistent CTAs (two per SM) walk the work
+// items (column pair, n2).  The pair's raw row x = (a, b) (N1 x 16 B,
+// contiguous in the perm layout) arrives in shared memory by one bulk copy
+// issued while the previous item's last residue is still transforming; the
+// weighted input z = x n is formed in place once per item (the loss column
+// sums fall out of that pass) and every residue reads it from shared memory
+// instead of re-reading the columns through L1/L2.  To fit z (N1 x 16 B) and
+// the transform's exchange in two CTAs per SM, exchanges go through a
+// half-size buffer in two rounds (fft_fwd_split).
+template <int N1>
+__global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs a, int nitems) {
+  constexpr int E = fft_e(N1), T = fft_t(N1);
+  constexpr int NW = T / 32;
+  constexpr unsigned ROW_BYTES = N1 * sizeof(double2);
+  constexpr int NCHUNK = ROW_BYTES > 32768 ? ROW_BYTES / 32768 : 1;
+  static_assert(T >= 64, "block transforms");
+  extern __shared__ __align__(128) double2 smem[];
+  double2* zs = smem;                                  // N1 slots: the item's x, then z
+  double* ex = reinterpret_cast<double*>(smem + N1);  // fft_smem_elems(N1) doubles
+  double2* stw = reinterpret_cast<double2*>(ex + ((fft_smem_elems(N1) + 1) & ~1));  // stage twiddles
+  __shared__ double red[2][NW];
+  __shared__ double2 Pst[2][16];
+  __shared__ double2 Ust[2][MAXRES];
+  __shared__ double2 Kst[MAXRES][16];
+  __shared__ __align__(8) uint64_t mbar;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int d = a.d;
+  const int N2 = a.N2;
+  const int K = d * N1;
+  const size_t Np = (size_t)N1 * N2;
+  const double2* X2 = reinterpret_cast<const double2*>(a.X);
+  for (int i = t; i < d * 16; i += T) {
+    const int j = i / 16, r = i % 16;
+    const cplx w = ld_c(a.tabK + (j * T * r) % K);
+    Kst[j][r] = make_double2(w.x, w.y);
+  }
+  fft_stage_table<N1>(stw, a.tw, t, T);
+  auto issue = [&](int it) {  // one thread: bulk-copy item it's row into zs
+    const int pair = a.pair0 + it / N2, n2 = it % N2;
+    const double2* src = X2 + (size_t)pair * Np + (size_t)n2 * N1;
+    fence_proxy_async();
+    mbar_expect_tx(&mbar, ROW_BYTES);
+#pragma unroll
+    for (int c = 0; c < NCHUNK; ++c)
+      bulk_g2s(zs + c * (N1 / NCHUNK), src + c * (N1 / NCHUNK), ROW_BYTES / NCHUNK, &mbar);
+  };
+  if (t == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0 && (int)blockIdx.x < nitems) issue(blockIdx.x);
+  unsigned parity = 0;
+  const size_t plane = (size_t)a.K_rows * N2;
+  for (int item = blockIdx.x, it_n = 0; item < nitems; item += gridDim.x, ++it_n) {
+    const int pair = a.pair0 + item / N2, n2 = item % N2;
+    const size_t e0 = (size_t)n2 * N1;
+    const double* nv = a.nv + e0;
+    const double* kv = a.kv ? a.kv + e0 : nullptr;
+    const int pb = it_n & 1;
+    if (t < 16) {
+      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * t);
+      Pst[pb][t] = make_double2(w.x, w.y);
+    } else if (t < 16 + d) {
+      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * (t - 16));
+      Ust[pb][t - 16] = make_double2(w.x, w.y);
+    }
+    // emit twiddle W_L^(n2 (j + d t)) = W_L^(n2 d t) W_L^(n2 j)
+    const cplx ct = twL(a.tabLlo, a.tabLhi, (long long)n2 * (d * t));
+    PMOut o;
+    o.TP = a.T + (size_t)pair * 2 * plane + (size_t)n2 * a.K_rows;
+    o.TM = o.TP + plane;
+    o.cn2 = twL(a.tabLlo, a.tabLhi, (long long)n2 * K);
+    // the state weights of this n2 row (through L1; shared by every pair)
+    double wv[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int n1 = t + T * r;
+      double w = __ldg(nv + n1);
+      if (kv) w = __dadd_rn(w, __dmul_rn(a.alpha, __ldg(kv + n1)));
+      wv[r] = w;
+    }
+    mbar_wait(&mbar, parity);
+    parity ^= 1;
+    cplx z[E];
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int n1 = t + T * r;
+      const double2 x = zs[n1];
+      z[r] = mk(x.x * wv[r], x.y * wv[r]);
+      zs[n1] = make_double2(z[r].x, z[r].y);
+      sa += z[r].x;
+      sb += z[r].y;
+    }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) {
+      red[0][wid] = sa;
+      red[1][wid] = sb;
+    }
+    __syncthreads();  // z complete in zs, red and Pst[pb] visible
+    if (t == 0) {
+      double ta = 0.0, tb = 0.0;
+      for (int w = 0; w < NW; ++w) {
+        ta += red[0][w];
+        tb += red[1][w];
+      }
+      a.dots[(size_t)(2 * pair) * a.nblk + n2] = ta;
+      a.dots[(size_t)(2 * pair + 1) * a.nblk + n2] = tb;
+    }
+    const int next = item + gridDim.x;
+    if (!a.want_T) {
+      __syncthreads();  // every thread is done with zs (and red)
+      if (t == 0 && next < nitems) issue(next);
+      continue;
+    }
+    // residue 0 straight from the registers
+    fft_fwd_split<N1>(z, t, ex, a.tw, CtaSync(), stw);
+#pragma unroll
+    for (int r = 0; r < E; ++r) emit_pm(a, o, N1, d, 0, t + T * r, z[r], cmul(ct, lds_c(&Pst[pb][r])));
+    for (int j = 1; j < d; ++j) {
+      cplx v[E];
+      const cplx tb = ld_c(a.tabK + j * t);
+#pragma unroll
+      for (int r = 0; r < E; ++r) v[r] = cmul(lds_c(zs + t + T * r), cmul(tb, lds_c(&Kst[j][r])));
+      if (j == d - 1) {
+        __syncthreads();  // zs free: the next item's row can land while this residue transforms
+        if (t == 0 && next < nitems) issue(next);
+      }
+      fft_fwd_split<N1>(v, t, ex, a.tw, CtaSync(), stw);
+      const cplx b = cmul(ct, lds_c(&Ust[pb][j]));
+#pragma unroll
+      for (int r = 0; r < E; ++r) emit_pm(a, o, N1, d, j, t + T * r, v[r], cmul(b, lds_c(&Pst[pb][r])));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // pass B: row FFTs, spectral product / chain, inverse row FFTs
 // ---------------------------------------------------------------------------
@@ -494,12 +659,22 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // regions that double as the row FFTs' exchange buffers (P stage for FFT(P),
 // M stage for FFT(M)); a plane is re-armed as soon as its FFT has passed the
 // transform's last barrier.
-template <int N2, bool TT>
-__global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
+template <int N2, bool TT, bool TMA>
+__global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __grid_constant__ CUtensorMap tmT) {
   constexpr int E = fft_e(N2), T = fft_t(N2), SE = fft_smem_elems(N2);
   constexpr int ROWS = 128 / T;
   constexpr int STG = (ROWS * SE > E * 128) ? ROWS * SE : E * 128;
-  extern __shared__ double2 smem[];
+  static_assert(!TMA || (N2 == 256 && ROWS == 8 && STG % 8 == 0), "TMA staging: 8 rows x 256, 128-byte aligned");
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ __align__(8) uint64_t mbar;  // TMA: both planes of the next pair landed
+  unsigned parity = 0;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   const int tid = threadIdx.x;
   const int rl8 = tid & 7, t = (tid >> 3) % T, sub = (tid >> 3) / T;
   const int rloc = sub * 8 + rl8;
@@ -524,6 +699,23 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
 #pragma unroll
       for (int i = 0; i < E; ++i) cp_async16(stage + i * 128 + tid, src + (size_t)(t + T * i) * a.K_rows, valid);
       cp_async_commit();
+    };
+    // TMA: one thread moves both planes of pair p (8 rows x 256 n2 x 16 B
+    // each, the [n2][row] staging layout; rows past K_rows arrive as zeros)
+    auto fetch_tma = [&](int p) {
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&mbar, 2u * ROWS * N2 * sizeof(double2));
+#pragma unroll
+        for (int pl = 0; pl < 2; ++pl) {
+          double2* dst = pl ? stM : stP;
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                  smem_u32(dst)),
+              "l"(&tmT), "r"(2 * rb * ROWS), "r"(0), "r"(2 * p + pl), "r"(smem_u32(&mbar))
+              : "memory");
+        }
+      }
     };
     // CP: running product over the modes of one rank term.  TT: chain
     // accumulator of the current state (core, rn); the last group processed
@@ -580,14 +772,23 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
       }
     };
 
-    fetch(stP, a.p0, 0);
-    fetch(stM, a.p0, 1);
+    if constexpr (TMA) {
+      fetch_tma(a.p0);
+    } else {
+      fetch(stP, a.p0, 0);
+      fetch(stM, a.p0, 1);
+    }
     for (int p = a.p0; p < a.p1; ++p) {
       const bool more = p + 1 < a.p1;
       cplx vp[E], vm[E];
 #if TTAGG_B_JOINT
       if constexpr (N2 == 256) {
-        cp_async_wait<0>();
+        if constexpr (TMA) {
+          mbar_wait(&mbar, parity);
+          parity ^= 1;
+        } else {
+          cp_async_wait<0>();
+        }
 #pragma unroll
         for (int i = 0; i < E; ++i) {
           vp[i] = lds_c(stP + i * 128 + tid);
@@ -605,14 +806,19 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a) {
         }
         __syncthreads();
         fft_fwd2<N2>(vp, vm, t, stP + rloc * SE, stM + rloc * SE, a.tw);
-        if (more) {
-          fetch(stP, p + 1, 0);
-          fetch(stM, p + 1, 1);
+        if constexpr (TMA) {
+          if (more) fetch_tma(p + 1);  // every thread is past the transforms' last barrier
+          if constexpr (TT) cp_async_wait<0>();  // the state group
         } else {
-          cp_async_commit();
-          cp_async_commit();
+          if (more) {
+            fetch(stP, p + 1, 0);
+            fetch(stM, p + 1, 1);
+          } else {
+            cp_async_commit();
+            cp_async_commit();
+          }
+          if constexpr (TT) cp_async_wait<2>();  // the state group (P/M of p+1 may fly on)
         }
-        if constexpr (TT) cp_async_wait<2>();  // the state group (P/M of p+1 may fly on)
       } else
 #endif
       {
@@ -1259,16 +1465,47 @@ int set_smem(K kern, size_t bytes) {
 }
 
 // ---- pass A
+// 1: TMA-fed persistent pass A for N1 >= 1024 (default); 0: passA_big_kernel
+// (TTAGG_PASSA=0, kept for A/B measurements)
+int passA_mode() {
+  static const int mode = [] {
+    const char* e = getenv("TTAGG_PASSA");
+    return e ? atoi(e) : 1;
+  }();
+  return mode;
+}
+
 // columns per pass-A CTA: thread groups of <= 128 threads when the transform allows
 constexpr int passA_G(int T, int N2) { return std::max(1, std::min(256 / T, N2)); }
 
 template <int N1>
 int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   constexpr int T = fft_t(N1);
+  if constexpr (T >= 64) {
+    if (passA_mode() == 1) {
+      const size_t smem = (size_t)N1 * sizeof(double2) + (size_t)((fft_smem_elems(N1) + 1) & ~1) * sizeof(double) +
+                          (size_t)fft_stage_table_elems<N1>() * sizeof(double2);
+      TRY(set_smem(passA_tma_kernel<N1>, smem));
+      static int resident[64] = {0};  // CTAs per SM x SMs, per device
+      int dev = 0;
+      CUDA_TRY(cudaGetDevice(&dev));
+      if (dev >= 64) return fail(TTAGG_ERR_UNSUPPORTED, "device ordinal >= 64");
+      if (!resident[dev]) {
+        int sms = 0, occ = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passA_tma_kernel<N1>, T, smem));
+        resident[dev] = std::max(1, occ) * sms;
+      }
+      const int nitems = npairs * N2;
+      const int grid = std::max(1, std::min(nitems, resident[dev]));
+      passA_tma_kernel<N1><<<grid, T, smem, st>>>(a, nitems);
+      CUDA_TRY(cudaGetLastError());
+      return TTAGG_OK;
+    }
+  }
   if constexpr (T >= 32) {
     const size_t smem = (size_t)fft_smem_elems(N1) * sizeof(double2);
     TRY(set_smem(passA_big_kernel<N1>, smem));
-
     passA_big_kernel<N1><<<npairs * N2, T, smem, st>>>(a);
     CUDA_TRY(cudaGetLastError());
     return TTAGG_OK;
@@ -1302,7 +1539,7 @@ int dispatchA(int N1, const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
 }
 
 // ---- pass B
-template <int N2, bool TT>
+template <int N2>
 size_t smemB() {
   constexpr int T = fft_t(N2);
   constexpr int ROWS = 128 / T;
@@ -1311,21 +1548,70 @@ size_t smemB() {
 }
 
 template <int N2, bool TT>
-int launchB(const PassBArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = smemB<N2, TT>();
-  TRY(set_smem(passB_kernel<N2, TT>, smem));
-  passB_kernel<N2, TT><<<grid, 128, smem, st>>>(a);
+int launchB(const PassBArgs& a, const CUtensorMap* tm, int grid, cudaStream_t st) {
+  const size_t smem = smemB<N2>();
+  if constexpr (N2 == 256) {
+    if (tm) {
+      TRY(set_smem(passB_kernel<N2, TT, true>, smem));
+      passB_kernel<N2, TT, true><<<grid, 128, smem, st>>>(a, *tm);
+      CUDA_TRY(cudaGetLastError());
+      return TTAGG_OK;
+    }
+  }
+  CUtensorMap none;
+  std::memset(&none, 0, sizeof(none));
+  TRY(set_smem(passB_kernel<N2, TT, false>, smem));
+  passB_kernel<N2, TT, false><<<grid, 128, smem, st>>>(a, none);
   CUDA_TRY(cudaGetLastError());
   return TTAGG_OK;
 }
 
 int rowsB(int N2) { return 128 / fft_t(N2); }
 
+// 1: pass B streams the exchange with TMA tensor copies (N2 = 256, default);
+// 0: per-thread cp.async (TTAGG_PASSB_TMA=0, kept for A/B measurements)
+int passB_tma() {
+  static const int mode = [] {
+    const char* e = getenv("TTAGG_PASSB_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  return mode;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// The exchange T[pair][plane][n2][rho] (double2) as a 3-D fp64 tensor
+// {2 K_rows, N2, 2 npairs}; one box = 8 rows x all N2 of one plane.
+int exchange_tensor_map(CUtensorMap* tm, const double2* T, int K_rows, int N2, int npairs) {
+  static EncodeTiledFn encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = (EncodeTiledFn)fn;
+  });
+  if (!encode) return fail(TTAGG_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * K_rows, (cuuint64_t)N2, (cuuint64_t)2 * npairs};
+  const cuuint64_t strides[2] = {(cuuint64_t)K_rows * sizeof(double2), (cuuint64_t)K_rows * N2 * sizeof(double2)};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * rowsB(N2)), (cuuint32_t)N2, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)T, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TTAGG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return TTAGG_OK;
+}
+
 // N2 <= 256 always (make_geom): the row block is 8 rows of one 16-thread
 // row transform each (the lane map in passB_kernel assumes T <= 16)
-int dispatchB(int N2, bool tt, const PassBArgs& a, int grid, cudaStream_t st) {
+int dispatchB(int N2, bool tt, const PassBArgs& a, const CUtensorMap* tm, int grid, cudaStream_t st) {
 #define TTAGG_B(n) \
-  case n: return tt ? launchB<n, true>(a, grid, st) : launchB<n, false>(a, grid, st);
+  case n: return tt ? launchB<n, true>(a, tm, grid, st) : launchB<n, false>(a, tm, grid, st);
   switch (N2) {
     TTAGG_B(16)
     TTAGG_B(32)
@@ -1500,9 +1786,12 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
     TRY(ensure((void**)&w.scratch, &w.scratch_bytes, need));
     b.scratch = w.scratch;
   }
+  CUtensorMap tm;
+  const bool use_tma = g.N2 == 256 && passB_tma();
+  if (use_tma) TRY(exchange_tensor_map(&tm, w.T, P->K_rows, g.N2, k->C_pad / 2));
   {
     ProfScope ps(ctx, 1, st, k->d);
-    TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, gridB, st));
+    TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, use_tma ? &tm : nullptr, gridB, st));
     ++ctx->launches;
   }
   PassCArgs c{};
