@@ -283,6 +283,30 @@ __device__ __forceinline__ void emit_pm(const PassAArgs& a, const PMOut& o, int 
   }
 }
 
+// emit_pm with the plane known per register (block transforms, E = 16): the
+// outputs k1 = t + T r with r < 8 (k1 < N1/2) are P rows only, r >= 8 M rows
+// only, except k1 = 0 (also M, as conj(Y)) and, for residue 0, k1 = N1/2
+// (also P) — both held by thread 0.  The M value is formed as conj(Y) times
+// conj(w) cn2 = conj(b) PMst[r] (PMst[r] = conj(Pst[r]) cn2): two complex
+// multiplies per output instead of three.  Assumes res_cnt[0] = N1/2 + 1 and
+// res_cnt[j>0] = N1/2 (checked on the host).
+template <int N1>
+__device__ __forceinline__ void emit_split(const PassAArgs& a, const PMOut& o, int d, int j, int t, const cplx (&v)[16],
+                                           cplx b, const double2* Pst, const double2* PMst) {
+  constexpr int T = N1 / 16;
+  double2* TP = o.TP + a.res_base[j];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) sts_c(TP + t + T * r, cmul(v[r], cmul(b, lds_c(Pst + r))));
+  const cplx bc = cconj(b);
+  double2* TM = j == 0 ? o.TM + a.res_base[0] + N1 - t : o.TM + a.res_base[d - j] + (N1 - 1 - t);
+#pragma unroll
+  for (int r = 8; r < 16; ++r) sts_c(TM - T * r, cmul(cconj(v[r]), cmul(bc, lds_c(PMst + r))));
+  if (t == 0 && j == 0) {
+    sts_c(o.TM + a.res_base[0], cconj(v[0]));
+    sts_c(TP + T * 8, cmul(v[8], cmul(b, lds_c(Pst + 8))));
+  }
+}
+
 // Small column transforms (T < 32 threads per column): one CTA = one column
 // pair x G adjacent columns; residues transformed in sequence.
 template <int N1>
@@ -492,7 +516,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
   double* ex = reinterpret_cast<double*>(smem + N1);  // fft_smem_elems(N1) doubles
   double2* stw = reinterpret_cast<double2*>(ex + ((fft_smem_elems(N1) + 1) & ~1));  // stage twiddles
   __shared__ double red[2][NW];
-  __shared__ double2 Pst[2][16];
+  __shared__ double2 Pst[2][16], PMst[2][16];
   __shared__ double2 Ust[2][MAXRES];
   __shared__ double2 Kst[MAXRES][16];
   __shared__ __align__(8) uint64_t mbar;
@@ -544,6 +568,11 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
     o.TP = a.T + (size_t)pair * 2 * plane + (size_t)n2 * a.K_rows;
     o.TM = o.TP + plane;
     o.cn2 = twL(a.tabLlo, a.tabLhi, (long long)n2 * K);
+    if (t >= 32 && t < 48) {
+      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * (t - 32));
+      const cplx pm = cmul(cconj(w), o.cn2);
+      PMst[pb][t - 32] = make_double2(pm.x, pm.y);
+    }
     // the state weights of this n2 row (through L1; shared by every pair)
     double wv[E];
 #pragma unroll
@@ -590,8 +619,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
     }
     // residue 0 straight from the registers
     fft_fwd_split<N1>(z, t, ex, a.tw, CtaSync(), stw);
-#pragma unroll
-    for (int r = 0; r < E; ++r) emit_pm(a, o, N1, d, 0, t + T * r, z[r], cmul(ct, lds_c(&Pst[pb][r])));
+    emit_split<N1>(a, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
     for (int j = 1; j < d; ++j) {
       cplx v[E];
       const cplx tb = ld_c(a.tabK + j * t);
@@ -602,9 +630,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
         if (t == 0 && next < nitems) issue(next);
       }
       fft_fwd_split<N1>(v, t, ex, a.tw, CtaSync(), stw);
-      const cplx b = cmul(ct, lds_c(&Ust[pb][j]));
-#pragma unroll
-      for (int r = 0; r < E; ++r) emit_pm(a, o, N1, d, j, t + T * r, v[r], cmul(b, lds_c(&Pst[pb][r])));
+      emit_split<N1>(a, o, d, j, t, v, cmul(ct, lds_c(&Ust[pb][j])), Pst[pb], PMst[pb]);
     }
   }
 }
@@ -1482,7 +1508,9 @@ template <int N1>
 int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   constexpr int T = fft_t(N1);
   if constexpr (T >= 64) {
-    if (passA_mode() == 1) {
+    bool halves = true;  // emit_split's plane map (always true for the plans make_plan builds)
+    for (int j = 0; j < a.d; ++j) halves = halves && a.res_cnt[j] == N1 / 2 + (j == 0);
+    if (passA_mode() == 1 && halves) {
       const size_t smem = (size_t)N1 * sizeof(double2) + (size_t)((fft_smem_elems(N1) + 1) & ~1) * sizeof(double) +
                           (size_t)fft_stage_table_elems<N1>() * sizeof(double2);
       TRY(set_smem(passA_tma_kernel<N1>, smem));
