@@ -635,148 +635,6 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
   }
 }
 
-// Pass A, two thread groups per CTA (N1 = 4096; one CTA per SM): the groups
-// transform the residues of the SAME work item in alternation (the item's
-// "former" group takes j = 0, 2, 4, ..., the other j = 1, 3, ...), so the
-// weighted input z is formed once per item into shared memory and read from
-// there by every residue, while each group keeps a full 16-byte exchange
-// buffer (no split exchanges).  The former group builds z straight into the
-// registers of residue 0 (the row was prefetched into L2 one item ahead).
-// The groups hand the z buffer over with non-blocking named barriers: the
-// group that transforms the last residue arrives on "zs free" once it has
-// read its input, and the next item's former (the group that does NOT
-// transform the last residue) waits there before overwriting z; the former
-// arrives on "zs ready" once z is written, and the other group waits there
-// before its first residue.  Shared memory: z (64 KB) + 2 exchanges (2 x 70 KB)
-// + stage twiddles (9 KB).
-__device__ __forceinline__ void bar_arrive_n(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-template <int N1>
-__global__ void __launch_bounds__(2 * fft_t(N1), 1) passA_dual_kernel(const PassAArgs a, int nitems) {
-  constexpr int E = fft_e(N1), T = fft_t(N1), SE = fft_smem_elems(N1);
-  constexpr int NW = T / 32;
-  constexpr int BAR_FREE = 3, BAR_READY = 4;
-  static_assert(E == 16 && T >= 64, "block transforms");
-  extern __shared__ __align__(128) double2 smem[];
-  const int g = threadIdx.x / T, t = threadIdx.x % T, lane = t & 31, wid = t >> 5;
-  double2* zs = smem;
-  double2* exg = smem + N1 + g * SE;
-  double2* stw = smem + N1 + 2 * SE;
-  __shared__ double red[2][2][NW];
-  __shared__ double2 Pst[2][16], PMst[2][16], Ust[2][MAXRES];
-  __shared__ double2 Kst[MAXRES][16];
-  const GroupSync gs{1 + g, T};
-  const int d = a.d;
-  const int N2 = a.N2;
-  const int K = d * N1;
-  const size_t Np = (size_t)N1 * N2;
-  const double2* X2 = reinterpret_cast<const double2*>(a.X);
-  for (int i = threadIdx.x; i < d * 16; i += 2 * T) {
-    const int j = i / 16, r = i % 16;
-    const cplx w = ld_c(a.tabK + (j * T * r) % K);
-    Kst[j][r] = make_double2(w.x, w.y);
-  }
-  fft_stage_table<N1>(stw, a.tw, threadIdx.x, 2 * T);
-  auto row_of = [&](int it) { return X2 + (size_t)(a.pair0 + it / N2) * Np + (size_t)(it % N2) * N1; };
-  if (threadIdx.x == 0 && (int)blockIdx.x < nitems) prefetch_l2_bulk(row_of(blockIdx.x), N1 * sizeof(double2));
-  __syncthreads();
-  if (!a.want_T && g == 1) return;  // loss sums only: group 0 alone, no hand-over
-  const size_t plane = (size_t)a.K_rows * N2;
-  int former = 0;
-  for (int item = blockIdx.x, k = 0; item < nitems; item += gridDim.x, ++k) {
-    const int pair = a.pair0 + item / N2, n2 = item % N2;
-    const int pb = k & 1;
-    const bool is_former = g == former;
-    const bool more = item + (int)gridDim.x < nitems;
-    PMOut o;
-    o.TP = a.T + (size_t)pair * 2 * plane + (size_t)n2 * a.K_rows;
-    o.TM = o.TP + plane;
-    o.cn2 = twL(a.tabLlo, a.tabLhi, (long long)n2 * K);
-    const cplx ct = twL(a.tabLlo, a.tabLhi, (long long)n2 * (d * t));
-    int j0;
-    if (is_former) {
-      if (t == 0 && more) prefetch_l2_bulk(row_of(item + gridDim.x), N1 * sizeof(double2));
-      const size_t e0 = (size_t)n2 * N1;
-      const double2* xp = X2 + (size_t)pair * Np + e0;
-      const double* nv = a.nv + e0;
-      const double* kv = a.kv ? a.kv + e0 : nullptr;
-      cplx z[E];
-#pragma unroll
-      for (int r = 0; r < E; ++r) {
-        const int n1 = t + T * r;
-        double w = __ldg(nv + n1);
-        if (kv) w = __dadd_rn(w, __dmul_rn(a.alpha, __ldg(kv + n1)));
-        const double2 x = __ldg(xp + n1);
-        z[r] = mk(x.x * w, x.y * w);
-      }
-      if (k > 0 && a.want_T) bar_sync_n(BAR_FREE, 2 * T);  // every residue input of the previous item has been read
-      double sa = 0.0, sb = 0.0;
-#pragma unroll
-      for (int r = 0; r < E; ++r) {
-        zs[t + T * r] = make_double2(z[r].x, z[r].y);
-        sa += z[r].x;
-        sb += z[r].y;
-      }
-      if (t < 16) {
-        const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * t);
-        Pst[pb][t] = make_double2(w.x, w.y);
-        const cplx pm = cmul(cconj(w), o.cn2);
-        PMst[pb][t] = make_double2(pm.x, pm.y);
-      } else if (t < 16 + d) {
-        const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * (t - 16));
-        Ust[pb][t - 16] = make_double2(w.x, w.y);
-      }
-      sa = warp_sum(sa);
-      sb = warp_sum(sb);
-      if (lane == 0) {
-        red[g][0][wid] = sa;
-        red[g][1][wid] = sb;
-      }
-      if (a.want_T) {
-        __threadfence_block();
-        bar_arrive_n(BAR_READY, 2 * T);  // z and this item's twiddles are in shared memory
-      }
-      gs();
-      if (t == 0) {
-        double ta = 0.0, tb = 0.0;
-        for (int w = 0; w < NW; ++w) {
-          ta += red[g][0][w];
-          tb += red[g][1][w];
-        }
-        a.dots[(size_t)(2 * pair) * a.nblk + n2] = ta;
-        a.dots[(size_t)(2 * pair + 1) * a.nblk + n2] = tb;
-      }
-      if (!a.want_T) continue;
-      fft_fwd<N1, GroupSync>(z, t, exg, a.tw, gs, stw);
-      emit_split<N1>(a, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
-      j0 = 2;
-    } else {
-      bar_sync_n(BAR_READY, 2 * T);
-      j0 = 1;
-    }
-    for (int j = j0; j < d; j += 2) {
-      cplx v[E];
-      const cplx tb = ld_c(a.tabK + j * t);
-#pragma unroll
-      for (int r = 0; r < E; ++r) v[r] = cmul(lds_c(zs + t + T * r), cmul(tb, lds_c(&Kst[j][r])));
-      if (j == d - 1 && more) {
-        __threadfence_block();
-        bar_arrive_n(BAR_FREE, 2 * T);
-      }
-      fft_fwd<N1, GroupSync>(v, t, exg, a.tw, gs, stw);
-      emit_split<N1>(a, o, d, j, t, v, cmul(ct, lds_c(&Ust[pb][j])), Pst[pb], PMst[pb]);
-    }
-    // the next former is the group that did not transform residue d-1
-    if (d % 2 == 1) former = 1 - former;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // pass B: row FFTs, spectral product / chain, inverse row FFTs
 // ---------------------------------------------------------------------------
@@ -1652,21 +1510,6 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
   if constexpr (T >= 64) {
     bool halves = true;  // emit_split's plane map (always true for the plans make_plan builds)
     for (int j = 0; j < a.d; ++j) halves = halves && a.res_cnt[j] == N1 / 2 + (j == 0);
-    if constexpr (N1 == 4096) {
-      if (passA_mode() == 3 && halves) {
-        const size_t smem = (size_t)(N1 + 2 * fft_smem_elems(N1) + fft_stage_table_elems<N1>()) * sizeof(double2);
-        TRY(set_smem(passA_dual_kernel<N1>, smem));
-        static int sms[64] = {0};
-        int dev = 0;
-        CUDA_TRY(cudaGetDevice(&dev));
-        if (dev >= 64) return fail(TTAGG_ERR_UNSUPPORTED, "device ordinal >= 64");
-        if (!sms[dev]) CUDA_TRY(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
-        const int nitems = npairs * N2;
-        passA_dual_kernel<N1><<<std::max(1, std::min(nitems, sms[dev])), 2 * T, smem, st>>>(a, nitems);
-        CUDA_TRY(cudaGetLastError());
-        return TTAGG_OK;
-      }
-    }
     if (passA_mode() == 1 && halves) {
       const size_t smem = (size_t)N1 * sizeof(double2) + (size_t)((fft_smem_elems(N1) + 1) & ~1) * sizeof(double) +
                           (size_t)fft_stage_table_elems<N1>() * sizeof(double2);
