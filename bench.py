@@ -170,7 +170,12 @@ def cpu_sample_desc(factors_by_order, workers):
 
 
 def run_reference(args, N, factors_by_order, n0):
+    """The reference arm: whole C5 RHS evaluations on the host cores.  One
+    whole RHS (≈23 s on the box's 16 cores) warms scipy's plan cache and the
+    page-ins; more warm-up would only lengthen the run (the line reports the
+    warm-up actually run)."""
     workers = os.cpu_count() or 1
+    args.warmup = min(args.warmup, 1)
     for _ in range(args.warmup):
         cpu_whole_rhs(factors_by_order, n0, workers)
     times = [cpu_whole_rhs(factors_by_order, n0, workers) for _ in range(args.steps)]

@@ -151,6 +151,14 @@ int ttagg_profile_read(ttagg_ctx* ctx, double* out72);
  * ttagg_rhs_perm (monotone counter; the bench reports the difference). */
 int ttagg_launch_count(ttagg_ctx* ctx, int64_t* out);
 
+/* Debug (no reference counterpart): with on = 1 every scratch buffer the
+ * context uses (exchange, inverse rows, TT chain state, per-order gains,
+ * column sums, loss coefficients) is filled with NaN bytes on the call's
+ * stream before use, so any read of a value the call did not write first
+ * shows up as a non-finite result.  The bounds/initialisation check that
+ * stands in for compute-sanitizer initcheck (tests/test_gpu_guard.py). */
+int ttagg_debug_poison(ttagg_ctx* ctx, int on);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,7 @@ _SIGNATURES = {
     "ttagg_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ttagg_profile_read": (ctypes.c_int, [_vp, _c_double_p]),
     "ttagg_launch_count": (ctypes.c_int, [_vp, _c_int64_p]),
+    "ttagg_debug_poison": (ctypes.c_int, [_vp, ctypes.c_int]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -340,6 +341,10 @@ class Context:
 
     def profile(self, on: bool):
         check(load().ttagg_profile_enable(self.handle, 1 if on else 0), "ttagg_profile_enable")
+
+    def debug_poison(self, on: bool):
+        """NaN-fill every scratch buffer before use (initialisation check, ttagg_debug_poison)."""
+        check(load().ttagg_debug_poison(self.handle, int(bool(on))), "ttagg_debug_poison")
 
     def launch_count(self) -> int:
         out = ctypes.c_int64(0)

@@ -172,6 +172,7 @@ struct ttagg_ctx {
   std::vector<Rec> recs;
   double prof_acc[5] = {0, 0, 0, 0, 0};
   long long launches = 0;  // kernel launches issued by this context
+  bool poison = false;     // debug: NaN-fill every scratch buffer before use
   // the workspaces above are shared by every call: the GPU work of a call
   // issued on one stream waits for the previous call's (on any other stream)
   cudaEvent_t ev_last = nullptr;
@@ -1723,6 +1724,14 @@ int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
     const size_t need = (size_t)k->C_pad * P->K_rows * g.N2 * sizeof(double2);
     TRY(ensure((void**)&w.T, &w.T_bytes, need, true));
     TRY(ensure((void**)&w.U, &w.U_bytes, (size_t)P->K_rows * g.N2 * sizeof(double2)));
+    if (ctx->poison) {
+      CUDA_TRY(cudaMemsetAsync(w.T, 0xFF, w.T_bytes, st));
+      CUDA_TRY(cudaMemsetAsync(w.U, 0xFF, w.U_bytes, st));
+    }
+  }
+  if (ctx->poison) {
+    CUDA_TRY(cudaMemsetAsync(k->dots, 0xFF, (size_t)std::max(2, k->C_pad) * k->nblk * sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(k->coef, 0xFF, (size_t)std::max(1, k->ntail) * sizeof(double), st));
   }
   PassAArgs a{};
   a.X = k->X;
@@ -1812,6 +1821,7 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
     if (per_sm > 0 && ctx->num_sms > 0) gridB = std::min(gridB, per_sm * ctx->num_sms);
     const size_t need = (size_t)gridB * 2 * k->Rmax * fft_e(g.N2) * 128 * sizeof(double2);
     TRY(ensure((void**)&w.scratch, &w.scratch_bytes, need));
+    if (ctx->poison) CUDA_TRY(cudaMemsetAsync(w.scratch, 0xFF, w.scratch_bytes, st));
     b.scratch = w.scratch;
   }
   CUtensorMap tm;
@@ -1993,6 +2003,7 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
                double alpha, bool wantP, bool wantQ, CombineArgs* A, cudaStream_t st) {
   const Geom& g = ks[0]->g;
   if (wantP) TRY(ensure((void**)&ctx->pbuf, &ctx->pbuf_bytes, (size_t)nk * g.Np * sizeof(double)));
+  if (wantP && ctx->poison) CUDA_TRY(cudaMemsetAsync(ctx->pbuf, 0xFF, ctx->pbuf_bytes, st));
   auto pslot = [&](int i) { return wantP ? ctx->pbuf + (size_t)i * g.Np : nullptr; };
   std::vector<int> order;  // FFT-route orders (CP / TT), costliest first
   for (int i = 0; i < nk; ++i) {
@@ -2802,6 +2813,12 @@ int ttagg_rk2(ttagg_ctx* ctx, const ttagg_kernel* const* kernels, int n_kernels,
 int ttagg_profile_enable(ttagg_ctx* ctx, int on) {
   if (!ctx) return fail(TTAGG_ERR_ARG, "null ctx");
   ctx->prof = on != 0;
+  return TTAGG_OK;
+}
+
+int ttagg_debug_poison(ttagg_ctx* ctx, int on) {
+  if (!ctx) return fail(TTAGG_ERR_ARG, "null argument");
+  ctx->poison = on != 0;
   return TTAGG_OK;
 }
 
