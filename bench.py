@@ -312,8 +312,18 @@ def extras(ctx, dev, stream, peak, steps):
         return bytes_ / (ms * 1e-3) / 1e9 / peak
 
     c5 = CONFIGS["C5"]
-    # D = 4 at N = 2^20 (orders 2..4, CP ranks 2/6/24, the C5 exponents / state)
     N = 1 << 20
+    # opt-in deduplication (ttagg_cp_upload_dedup) on the C5 tensor itself: the
+    # permutation-power factors hold d distinct vectors per order, so pass A
+    # transforms <= d^2 distinct column pairs instead of d R / 2; same results
+    # (bitwise), reported apart from the headline (which evaluates every rank term)
+    dks = [ctx.upload_cp(permutation_power_cp(c5.exponents[:d], N), dedup=True) for d in c5.orders]
+    ms = _timed_rhs(ctx, dks, initial_state("c5", N), dev, stream, steps)
+    out["c5_dedup"] = {"rhs_per_s": 1e3 / ms, "ms_per_rhs": ms,
+                       "workload": "C5 tensor (D=5, N=2^20, CP ranks 2/6/24/120) with identical factor columns "
+                                   "stored and transformed once (opt-in; same RHS bitwise)"}
+    del dks
+    # D = 4 at N = 2^20 (orders 2..4, CP ranks 2/6/24, the C5 exponents / state)
     ks, dks, B = cp_set(c5.exponents, (2, 3, 4), N)
     ms = _timed_rhs(ctx, dks, initial_state("c5", N), dev, stream, steps)
     out["d4_n2p20"] = {"rhs_per_s": 1e3 / ms, "ms_per_rhs": ms, "model_frac": frac(B, ms),

@@ -70,6 +70,17 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank,
                     const double* const* factors, const int64_t* rank_subset,
                     int64_t n_subset, ttagg_kernel** out);
 
+/* Opt-in variant (no reference counterpart): identical
+ * factor columns (bitwise) are stored and transformed once — every distinct
+ * ordered pair of columns gets one exchange slot that pass B reads for each
+ * pair mapping to it, identical tail columns share one row.  Same results
+ * as ttagg_cp_upload (the rank/mode structure is unchanged); for kernels
+ * built from few distinct vectors (the permutation-power and Brownian
+ * families) the column transforms shrink accordingly. */
+int ttagg_cp_upload_dedup(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank,
+                          const double* const* factors, const int64_t* rank_subset,
+                          int64_t n_subset, ttagg_kernel** out);
+
 /* Upload a TT kernel (replaces TTKernel, kernels.py:137-180, plus the fiber
  * layout of rhs_tt_P, rhs.py:256-269).  ranks: d+1 entries with
  * ranks[0] == ranks[d] == 1; cores: d host pointers, core l of shape

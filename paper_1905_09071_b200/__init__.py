@@ -72,7 +72,23 @@ __all__ = [
     "SERIAL_PLAN",
     "lpt_rank_shards",
     "install",
+    "dedup_identical_columns",
 ]
+
+
+def dedup_identical_columns(enabled: bool = True) -> bool:
+    """Opt-in storage mode for CP kernels (no reference counterpart): identical
+    factor columns are uploaded and transformed once (ttagg_cp_upload_dedup).
+    Results are unchanged; kernels built from a few distinct vectors (the
+    permutation-power / Brownian families) get much cheaper column
+    transforms.  Off by default, so a rank-R kernel is evaluated as the R
+    rank terms it is specified as.  Applies to kernels uploaded after the
+    call; returns the previous setting."""
+    from . import _lib
+
+    prev = _lib.DEDUP
+    _lib.DEDUP = bool(enabled)
+    return prev
 
 
 def install(ttagg_module=None):

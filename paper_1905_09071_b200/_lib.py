@@ -61,6 +61,11 @@ _SIGNATURES = {
         [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(_vp), _c_int64_p,
          ctypes.c_int64, ctypes.POINTER(_vp)],
     ),
+    "ttagg_cp_upload_dedup": (
+        ctypes.c_int,
+        [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(_vp), _c_int64_p,
+         ctypes.c_int64, ctypes.POINTER(_vp)],
+    ),
     "ttagg_tt_upload": (
         ctypes.c_int,
         [_vp, ctypes.c_int, ctypes.c_int64, _c_int64_p, ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
@@ -98,6 +103,9 @@ EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
 _LIB = None
 _LOCK = threading.RLock()
+# opt-in: CP kernels are uploaded with identical columns deduplicated
+# (ttagg_cp_upload_dedup); set through paper_1905_09071_b200.dedup_identical_columns
+DEDUP = False
 
 
 def load():
@@ -186,7 +194,7 @@ class Context:
         self._lock = threading.RLock()
 
     # -- uploads -----------------------------------------------------------
-    def upload_cp(self, factors, rank_subset=None) -> DeviceKernel:
+    def upload_cp(self, factors, rank_subset=None, dedup=False) -> DeviceKernel:
         lib = load()
         fs = [np.ascontiguousarray(f, dtype=np.float64) for f in factors]
         d = len(fs)
@@ -199,10 +207,8 @@ class Context:
         else:
             sub_p, n_sub = None, 0
         h = _vp()
-        check(
-            lib.ttagg_cp_upload(self.handle, d, n_classes, rank, ptrs, sub_p, n_sub, ctypes.byref(h)),
-            "ttagg_cp_upload",
-        )
+        fn = "ttagg_cp_upload_dedup" if dedup else "ttagg_cp_upload"
+        check(getattr(lib, fn)(self.handle, d, n_classes, rank, ptrs, sub_p, n_sub, ctypes.byref(h)), fn)
         return DeviceKernel(self, h, KIND_CP, d, n_classes)
 
     def upload_tt(self, cores) -> DeviceKernel:
@@ -231,13 +237,14 @@ class Context:
 
     def device_kernel(self, kernel, rank_subset=None) -> DeviceKernel:
         """Upload once per (immutable) kernel object; cached by identity (kernels.py:129-134)."""
-        key = (id(kernel), None if rank_subset is None else tuple(int(r) for r in rank_subset))
+        dedup = DEDUP and hasattr(kernel, "factors")
+        key = (id(kernel), None if rank_subset is None else tuple(int(r) for r in rank_subset), dedup)
         with self._lock:
             hit = self._cache.get(key)
             if hit is not None and hit[0]() is kernel:
                 return hit[1]
             if hasattr(kernel, "factors"):
-                dk = self.upload_cp(kernel.factors, rank_subset)
+                dk = self.upload_cp(kernel.factors, rank_subset, dedup=dedup)
             elif hasattr(kernel, "cores"):
                 if rank_subset is not None:
                     raise NotImplementedError("rank sharding of TT kernels")

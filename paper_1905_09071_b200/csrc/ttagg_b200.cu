@@ -208,6 +208,13 @@ struct ttagg_kernel {
   double* dots = nullptr;
   double* coef = nullptr;
   OrderPlan* plan = nullptr;
+  // column pairs stored in X (pass A transforms these); without deduplication
+  // xpairs = C_pad / 2 and pair p lives at p.  Deduplicated CP uploads store
+  // each distinct (ordered) pair of columns once: pmap[p] is the stored pair
+  // of original pair p, dslot[c] the column-sum slot of original column c.
+  int xpairs = 0;
+  int* pmap = nullptr;
+  int* dslot = nullptr;
 };
 
 namespace {
@@ -653,6 +660,7 @@ struct PassBArgs {
   int nrb;           // row blocks (CTAs loop over them)
   int ranks[MAXD + 1];
   const int* fdesc;  // TT: per uploaded fiber, packed (core, rn, rp, first, last, noop)
+  const int* pmap;   // deduplicated CP: stored exchange pair of each pair (null: identity)
 };
 
 // TT fiber descriptor: the uploaded columns are the live fibers only (all-zero
@@ -721,8 +729,9 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
     const int rho = rb * ROWS + rloc;
     const bool valid = rho < a.K_rows;
     const double2* Tb = a.T + (valid ? rho : 0);  // + pair*2*plane + {0, plane} + n2*K_rows
+    auto xp = [&](int p) { return a.pmap ? __ldg(a.pmap + p) : p; };
     auto fetch = [&](double2* stage, int p, int pl) {
-      const double2* src = Tb + ((size_t)p * 2 + pl) * plane;
+      const double2* src = Tb + ((size_t)xp(p) * 2 + pl) * plane;
 #pragma unroll
       for (int i = 0; i < E; ++i) cp_async16(stage + i * 128 + tid, src + (size_t)(t + T * i) * a.K_rows, valid);
       cp_async_commit();
@@ -739,7 +748,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
           asm volatile(
               "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
                   smem_u32(dst)),
-              "l"(&tmT), "r"(2 * rb * ROWS), "r"(0), "r"(2 * p + pl), "r"(smem_u32(&mbar))
+              "l"(&tmT), "r"(2 * rb * ROWS), "r"(0), "r"(2 * xp(p) + pl), "r"(smem_u32(&mbar))
               : "memory");
         }
       }
@@ -962,6 +971,7 @@ struct QArgs {
   int ranks[MAXD + 1];
   int core_off[MAXD + 1];
   const int* cidx;  // TT: full fiber index -> uploaded column, -1 if dropped (contributes 0)
+  const int* dslot; // deduplicated CP: column-sum slot of each column (null: identity)
 };
 
 __global__ void __launch_bounds__(1024) qcoef_kernel(const QArgs a) {
@@ -971,7 +981,7 @@ __global__ void __launch_bounds__(1024) qcoef_kernel(const QArgs a) {
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int c = threadIdx.x >> 5; c < a.C; c += nw) {
     double s = 0.0;
-    const double* p = a.dots + (size_t)c * a.nblk;
+    const double* p = a.dots + (size_t)(a.dslot ? __ldg(a.dslot + c) : c) * a.nblk;
     for (int b = lane; b < a.nblk; b += 32) s += p[b];
     s = warp_sum(s);
     if (lane == 0) sdot[c] = s;
@@ -1718,10 +1728,10 @@ int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
               bool wantQ, ttagg_ctx::Work& w, cudaStream_t st) {
   const OrderPlan* P = k->plan;
   const Geom& g = k->g;
-  const int npairs = k->C_pad / 2;
+  const int npairs = k->xpairs;
   if (npairs > 65535) return fail(TTAGG_ERR_UNSUPPORTED, "too many columns for one kernel");
   if (wantP) {
-    const size_t need = (size_t)k->C_pad * P->K_rows * g.N2 * sizeof(double2);
+    const size_t need = (size_t)std::max(1, 2 * npairs) * P->K_rows * g.N2 * sizeof(double2);
     TRY(ensure((void**)&w.T, &w.T_bytes, need, true));
     TRY(ensure((void**)&w.U, &w.U_bytes, (size_t)P->K_rows * g.N2 * sizeof(double2)));
     if (ctx->poison) {
@@ -1773,6 +1783,7 @@ int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
       q.core_off[i] = k->core_off[i];
     }
     q.cidx = k->cidx;
+    q.dslot = k->dslot;
     ProfScope ps(ctx, 3, st, k->d);
     const size_t qsm = std::max(1, k->C_pad) * sizeof(double);
     TRY(set_smem(qcoef_kernel, qsm));
@@ -1803,6 +1814,7 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
   b.Rmax = k->Rmax;
   for (int i = 0; i <= MAXD; ++i) b.ranks[i] = k->ranks[i];
   b.fdesc = k->fdesc;
+  b.pmap = k->pmap;
   const int rows = rowsB(g.N2);
   b.nrb = (P->K_rows + rows - 1) / rows;
   b.p0 = 0;
@@ -1826,7 +1838,7 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
   }
   CUtensorMap tm;
   const bool use_tma = g.N2 == 256 && passB_tma();
-  if (use_tma) TRY(exchange_tensor_map(&tm, w.T, P->K_rows, g.N2, k->C_pad / 2));
+  if (use_tma) TRY(exchange_tensor_map(&tm, w.T, P->K_rows, g.N2, std::max(1, k->xpairs)));
   {
     ProfScope ps(ctx, 1, st, k->d);
     TRY(dispatchB(g.N2, k->kind == TTAGG_KIND_TT, b, use_tma ? &tm : nullptr, gridB, st));
@@ -2189,7 +2201,7 @@ static void release_kernel(ttagg_kernel* k) {
   cudaSetDevice(k->ctx->device);
   cudaDeviceSynchronize();
   for (void* p : {(void*)k->X, (void*)k->Xt, (void*)k->tail_cols, (void*)k->dots, (void*)k->coef, (void*)k->fdesc,
-                  (void*)k->cidx, (void*)k->V, (void*)k->nat, (void*)k->part})
+                  (void*)k->cidx, (void*)k->V, (void*)k->nat, (void*)k->part, (void*)k->pmap, (void*)k->dslot})
     cudaFree(p);
   delete k;
 }
@@ -2205,6 +2217,7 @@ struct KernelGuard {
 };
 
 static int finish_upload(ttagg_ctx* ctx, ttagg_kernel* k, const std::vector<int>& tails) {
+  if (!k->pmap) k->xpairs = k->C_pad / 2;
   k->ntail = (int)tails.size();
   CUDA_TRY(cudaMalloc(&k->tail_cols, std::max<size_t>(1, tails.size()) * sizeof(int)));
   if (!tails.empty())
@@ -2216,8 +2229,11 @@ static int finish_upload(ttagg_ctx* ctx, ttagg_kernel* k, const std::vector<int>
   return TTAGG_OK;
 }
 
-int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, const double* const* factors,
-                    const int64_t* rank_subset, int64_t n_subset, ttagg_kernel** out) {
+static int cp_upload_dedup(ttagg_ctx* ctx, ttagg_kernel* k, const double* const* factors, int64_t rank,
+                           const std::vector<int>& sel, std::vector<int>& tails);
+
+static int cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, const double* const* factors,
+                     const int64_t* rank_subset, int64_t n_subset, bool dedup, ttagg_kernel** out) {
   if (!ctx || !out || !factors) return fail(TTAGG_ERR_ARG, "null argument");
   if (d < 2) return fail(TTAGG_ERR_ARG, "a CP kernel needs at least two factors");
   if (d > MAXD) return fail(TTAGG_ERR_UNSUPPORTED, "collision order above 8");
@@ -2247,6 +2263,15 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
   k->C_pad = (k->C + 1) & ~1;
   k->Rmax = 1;
   const size_t colbytes = (size_t)g.Np * sizeof(double);
+  if (dedup) {
+    for (int m = 0; m < d; ++m)
+      if (!factors[m]) return fail(TTAGG_ERR_ARG, "null factor");
+    std::vector<int> tails;
+    TRY(cp_upload_dedup(ctx, k, factors, rank, sel, tails));
+    TRY(finish_upload(ctx, k, tails));
+    *out = guard.release();
+    return TTAGG_OK;
+  }
   {
     cudaError_t e = cudaMalloc(&k->X, std::max<size_t>(2, k->C_pad) * colbytes);
     if (e != cudaSuccess) {
@@ -2286,6 +2311,145 @@ int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, cons
   }
   TRY(finish_upload(ctx, k, tails));
   *out = guard.release();
+  return TTAGG_OK;
+}
+
+int ttagg_cp_upload(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, const double* const* factors,
+                    const int64_t* rank_subset, int64_t n_subset, ttagg_kernel** out) {
+  return cp_upload(ctx, d, n_classes, rank, factors, rank_subset, n_subset, false, out);
+}
+
+int ttagg_cp_upload_dedup(ttagg_ctx* ctx, int d, int64_t n_classes, int64_t rank, const double* const* factors,
+                          const int64_t* rank_subset, int64_t n_subset, ttagg_kernel** out) {
+  return cp_upload(ctx, d, n_classes, rank, factors, rank_subset, n_subset, true, out);
+}
+
+// Deduplicated CP upload: identical factor columns (bitwise) are found on the
+// host (FNV-1a hash per column, then a full comparison with the group's
+// representative).  Column c = j d + m of the rank-major order keeps its
+// place in the rank/mode structure pass B walks; only the storage changes:
+// every distinct ordered pair (column 2p, column 2p+1) is stored and
+// transformed once (pmap), the column sums are read from the stored pair's
+// slots (dslot), and identical tail columns share one row of Xt.
+static int cp_upload_dedup(ttagg_ctx* ctx, ttagg_kernel* k, const double* const* factors, int64_t rank,
+                           const std::vector<int>& sel, std::vector<int>& tails) {
+  const int d = k->d;
+  const int64_t N = k->N;
+  const int R = (int)sel.size();
+  const Geom& g = k->g;
+  // ---- column identities
+  std::vector<uint64_t> h((size_t)d * R, 1469598103934665603ull);
+  for (int m = 0; m < d; ++m)
+    for (int64_t i = 0; i < N; ++i) {
+      const double* row = factors[m] + i * rank;
+      for (int j = 0; j < R; ++j) {
+        uint64_t bits;
+        std::memcpy(&bits, row + sel[j], 8);
+        uint64_t& x = h[(size_t)m * R + j];
+        x = (x ^ bits) * 1099511628211ull;
+      }
+    }
+  auto same = [&](int m1, int j1, int m2, int j2) {
+    const double* a = factors[m1] + sel[j1];
+    const double* b = factors[m2] + sel[j2];
+    for (int64_t i = 0; i < N; ++i)
+      if (std::memcmp(a + i * rank, b + i * rank, 8) != 0) return false;
+    return true;
+  };
+  std::vector<int> col_id((size_t)k->C), rep_m, rep_j;
+  std::map<uint64_t, std::vector<int>> by_hash;  // hash -> distinct ids
+  for (int j = 0; j < R; ++j)
+    for (int m = 0; m < d; ++m) {
+      const uint64_t hv = h[(size_t)m * R + j];
+      int id = -1;
+      for (int cand : by_hash[hv])
+        if (same(rep_m[cand], rep_j[cand], m, j)) {
+          id = cand;
+          break;
+        }
+      if (id < 0) {
+        id = (int)rep_m.size();
+        rep_m.push_back(m);
+        rep_j.push_back(j);
+        by_hash[hv].push_back(id);
+      }
+      col_id[(size_t)j * d + m] = id;
+    }
+  // ---- distinct ordered pairs
+  std::map<std::pair<int, int>, int> pair_id;
+  std::vector<std::pair<int, int>> pairs;
+  std::vector<int> pmap(k->C_pad / 2), dslot(k->C);
+  for (int p = 0; p < k->C_pad / 2; ++p) {
+    const std::pair<int, int> key(col_id[2 * p], 2 * p + 1 < k->C ? col_id[2 * p + 1] : -1);
+    auto it = pair_id.find(key);
+    if (it == pair_id.end()) {
+      it = pair_id.emplace(key, (int)pairs.size()).first;
+      pairs.push_back(key);
+    }
+    pmap[p] = it->second;
+  }
+  for (int cc = 0; cc < k->C; ++cc) dslot[cc] = 2 * pmap[cc / 2] + (cc & 1);
+  k->xpairs = (int)pairs.size();
+  // ---- distinct tails (mode d-1 of every rank term)
+  std::map<int, int> tail_row;
+  std::vector<int> tail_rep;  // rank index j of each distinct tail
+  for (int j = 0; j < R; ++j) {
+    const int id = col_id[(size_t)j * d + d - 1];
+    auto it = tail_row.find(id);
+    if (it == tail_row.end()) {
+      it = tail_row.emplace(id, (int)tail_rep.size()).first;
+      tail_rep.push_back(j);
+    }
+    tails.push_back(it->second);
+  }
+  // ---- uploads
+  const size_t colbytes = (size_t)g.Np * sizeof(double);
+  CUDA_TRY(cudaMalloc(&k->X, (size_t)std::max(1, k->xpairs) * 2 * colbytes));
+  CUDA_TRY(cudaMemset(k->X, 0, (size_t)std::max(1, k->xpairs) * 2 * colbytes));
+  CUDA_TRY(cudaMalloc(&k->Xt, std::max<size_t>(1, tail_rep.size()) * colbytes));
+  CUDA_TRY(cudaMalloc(&k->pmap, pmap.size() * sizeof(int)));
+  CUDA_TRY(cudaMemcpy(k->pmap, pmap.data(), pmap.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&k->dslot, dslot.size() * sizeof(int)));
+  CUDA_TRY(cudaMemcpy(k->dslot, dslot.data(), dslot.size() * sizeof(int), cudaMemcpyHostToDevice));
+  Scratch sc;
+  CUDA_TRY(cudaMalloc(&sc.src, (size_t)N * rank * sizeof(double)));
+  const size_t nmax = (size_t)2 * pairs.size() + tail_rep.size() + 1;
+  CUDA_TRY(cudaMalloc(&sc.sel, nmax * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&sc.map, nmax * sizeof(int)));
+  for (int m = 0; m < d; ++m) {
+    std::vector<int> s, mp;  // source ranks, destination columns
+    for (size_t q = 0; q < pairs.size(); ++q)
+      for (int half = 0; half < 2; ++half) {
+        const int id = half ? pairs[q].second : pairs[q].first;
+        if (id >= 0 && rep_m[id] == m) {
+          s.push_back(sel[rep_j[id]]);
+          mp.push_back((int)(2 * q + half));
+        }
+      }
+    if (!s.empty()) {
+      CUDA_TRY(cudaMemcpy(sc.src, factors[m], (size_t)N * rank * sizeof(double), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(sc.sel, s.data(), s.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(sc.map, mp.data(), mp.size() * sizeof(int), cudaMemcpyHostToDevice));
+      dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)s.size());
+      scatter_columns_kernel<<<grid, 256>>>(sc.src, N, (int)rank, (int)s.size(), sc.sel, sc.map, k->X, g.N1, g.N2, 1);
+      CUDA_TRY(cudaGetLastError());
+    }
+    if (m == d - 1) {  // tails: the last factor's columns
+      std::vector<int> ts, tm;
+      for (size_t q = 0; q < tail_rep.size(); ++q) {
+        ts.push_back(sel[tail_rep[q]]);
+        tm.push_back((int)q);
+      }
+      if (s.empty()) CUDA_TRY(cudaMemcpy(sc.src, factors[m], (size_t)N * rank * sizeof(double), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(sc.sel, ts.data(), ts.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(sc.map, tm.data(), tm.size() * sizeof(int), cudaMemcpyHostToDevice));
+      dim3 grid((unsigned)std::min<int64_t>(1024, (g.Np + 255) / 256), (unsigned)ts.size());
+      scatter_columns_kernel<<<grid, 256>>>(sc.src, N, (int)rank, (int)ts.size(), sc.sel, sc.map, k->Xt, g.N1, g.N2,
+                                            0);
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaDeviceSynchronize());  // sc.src is reused by the next factor
+  }
   return TTAGG_OK;
 }
 
