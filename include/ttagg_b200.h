@@ -38,6 +38,7 @@ extern "C" {
 #define TTAGG_ERR_CUDA 5        /* CUDA runtime failure                                  */
 #define TTAGG_ERR_UNSUPPORTED 6 /* size or rank outside what this build handles          */
 #define TTAGG_ERR_NOMEM 7       /* device allocation failed                              */
+#define TTAGG_ERR_NCCL 8        /* NCCL failure (device groups)                          */
 
 /* flags */
 #define TTAGG_HOST_PTRS 1 /* n/p/q/s (rhs) or n/records (rk2) are host pointers      */
@@ -169,6 +170,29 @@ int ttagg_launch_count(ttagg_ctx* ctx, int64_t* out);
  * shows up as a non-finite result.  The bounds/initialisation check that
  * stands in for compute-sanitizer initcheck (tests/test_gpu_guard.py). */
 int ttagg_debug_poison(ttagg_ctx* ctx, int on);
+
+/* Device group (single process, several GPUs; SURVEY.md §8(e), §8(b)'s
+ * ttagg_ctx_create(devices, n)): one context per device plus an NCCL
+ * communicator (ncclCommInitAll; libnccl.so.2 is loaded at run time, and a
+ * one-device group needs none).  The caller uploads each device's kernel
+ * shard (CP rank subsets, TT slices of the first internal rank; a dense
+ * order on one device only) to ttagg_group_ctx(g, i) and passes them as an
+ * n_dev x n_kernels row-major table (null: that device holds no share of the
+ * order).  ttagg_group_rhs: host n in, host p/q/s out (each nullable), one
+ * all-reduce of the partial [p q s] per call.  ttagg_group_rk2: same
+ * contract as ttagg_rk2 with host pointers; per RHS one all-reduce of the
+ * partial dn/dt, then every device applies the identical stage update to
+ * its replica (integrator.py:153-228). */
+typedef struct ttagg_group ttagg_group;
+int ttagg_group_create(const int* devices, int n_dev, ttagg_group** out);
+int ttagg_group_destroy(ttagg_group* g);
+int ttagg_group_size(const ttagg_group* g, int* n_dev);
+int ttagg_group_ctx(ttagg_group* g, int i, ttagg_ctx** out);
+int ttagg_group_rhs(ttagg_group* g, const ttagg_kernel* const* kernels, int n_kernels,
+                    const double* n, double* p, double* q, double* s);
+int ttagg_group_rk2(ttagg_group* g, const ttagg_kernel* const* kernels, int n_kernels,
+                    double* n_inout, double t0, double dt, int64_t steps, int64_t record_every,
+                    double* records, int64_t* fail_step, int64_t* neg_step);
 
 #ifdef __cplusplus
 }

@@ -73,7 +73,20 @@ __all__ = [
     "lpt_rank_shards",
     "install",
     "dedup_identical_columns",
+    "use_devices",
 ]
+
+
+def use_devices(devices=None):
+    """Evaluate rhs_total / rhs_*_P/Q / integrate on several GPUs of this
+    process (a device group: rank-sharded kernels, one NCCL all-reduce per
+    RHS, ttagg_group_*).  ``None`` or ``[]`` returns to one device.  The
+    environment variable TTAGG_DEVICES="0,1,..." selects a group at first use,
+    so the reference's own CLI scales after install() without code changes.
+    Returns the group (or None)."""
+    from . import _lib
+
+    return _lib.set_group(list(devices) if devices else None)
 
 
 def dedup_identical_columns(enabled: bool = True) -> bool:

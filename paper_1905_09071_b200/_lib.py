@@ -38,6 +38,7 @@ TTAGG_ERR_NONFINITE = 4
 TTAGG_ERR_CUDA = 5
 TTAGG_ERR_UNSUPPORTED = 6
 TTAGG_ERR_NOMEM = 7
+TTAGG_ERR_NCCL = 8
 TTAGG_HOST_PTRS = 1
 TTAGG_WANT_P = 2
 TTAGG_WANT_Q = 4
@@ -98,6 +99,16 @@ _SIGNATURES = {
     "ttagg_profile_read": (ctypes.c_int, [_vp, _c_double_p]),
     "ttagg_launch_count": (ctypes.c_int, [_vp, _c_int64_p]),
     "ttagg_debug_poison": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "ttagg_group_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(_vp)]),
+    "ttagg_group_destroy": (ctypes.c_int, [_vp]),
+    "ttagg_group_size": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
+    "ttagg_group_ctx": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "ttagg_group_rhs": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "ttagg_group_rk2": (
+        ctypes.c_int,
+        [_vp, ctypes.POINTER(_vp), ctypes.c_int, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_int64,
+         ctypes.c_int64, _vp, _c_int64_p, _c_int64_p],
+    ),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -192,6 +203,16 @@ class Context:
         self.device = device
         self._cache = {}  # id(kernel object) -> (weakref, DeviceKernel)
         self._lock = threading.RLock()
+
+    @classmethod
+    def _wrap(cls, handle, device: int) -> "Context":
+        """A context owned by a device group (not destroyed through this object)."""
+        self = cls.__new__(cls)
+        self.handle = handle
+        self.device = device
+        self._cache = {}
+        self._lock = threading.RLock()
+        return self
 
     # -- uploads -----------------------------------------------------------
     def upload_cp(self, factors, rank_subset=None, dedup=False) -> DeviceKernel:
@@ -372,6 +393,140 @@ class Context:
 
 
 _CONTEXTS: dict[int, Context] = {}
+
+
+class Group:
+    """Several GPUs of this process as one rank-sharded engine (ttagg_group_*).
+
+    Each kernel object is split once into per-device shards — CP rank terms
+    by LPT (cost ~ d^2, rhs.py:375-381 is linear in the rank sum), TT cores by
+    slices of the first internal rank (construct.tt_rank_shard), a dense
+    order whole on the first device — and uploaded to that device's context;
+    every RHS is the all-reduced sum of the partials."""
+
+    def __init__(self, devices):
+        lib = load()
+        devs = [int(x) for x in devices]
+        if not devs:
+            raise ValueError("a device group needs at least one device")
+        arr = (ctypes.c_int * len(devs))(*devs)
+        h = _vp()
+        check(lib.ttagg_group_create(arr, len(devs), ctypes.byref(h)), "ttagg_group_create")
+        self.handle = h
+        self.devices = devs
+        self.ctxs = []
+        for i, dv in enumerate(devs):
+            c = _vp()
+            check(lib.ttagg_group_ctx(h, i, ctypes.byref(c)), "ttagg_group_ctx")
+            self.ctxs.append(Context._wrap(c, dv))
+        self._cache = {}
+        self._lock = threading.RLock()
+
+    def close(self):
+        if self.handle:
+            self._cache.clear()
+            for c in self.ctxs:
+                c._cache.clear()
+            import gc
+
+            gc.collect()
+            load().ttagg_group_destroy(self.handle)
+            self.handle = None
+
+    def shards(self, kernel):
+        """Per-device DeviceKernel (or None) for one kernel object, cached by identity."""
+        key = (id(kernel), DEDUP and hasattr(kernel, "factors"))
+        with self._lock:
+            hit = self._cache.get(key)
+            if hit is not None and hit[0]() is kernel:
+                return hit[1]
+            n = len(self.ctxs)
+            out = [None] * n
+            if hasattr(kernel, "factors"):
+                from .parallel import lpt_rank_shards
+
+                d = len(kernel.factors)
+                R = kernel.factors[0].shape[1]
+                shards = lpt_rank_shards({d: R}, n)
+                for i in range(n):
+                    sub = shards[(i + d) % n].get(d, [])  # rotate so small orders spread out
+                    if sub:
+                        out[i] = self.ctxs[i].upload_cp(kernel.factors, rank_subset=sub, dedup=key[1])
+            elif hasattr(kernel, "cores"):
+                from .construct import tt_rank_shard
+
+                for i in range(n):
+                    sl = tt_rank_shard(kernel.cores, n, i) if n > 1 else kernel.cores
+                    if sl is not None:
+                        out[i] = self.ctxs[i].upload_tt(sl)
+            elif hasattr(kernel, "values"):
+                out[0] = self.ctxs[0].upload_dense(kernel.values)
+            else:
+                from .kernels import KernelError
+
+                raise KernelError(f"unsupported kernel representation {type(kernel).__name__} on the GPU path")
+            try:
+                ref = weakref.ref(kernel, lambda _r, k=key: self._cache.pop(k, None))
+            except TypeError:
+                ref = lambda k=kernel: k  # noqa: E731
+            self._cache[key] = (ref, out)
+            return out
+
+    def _table(self, kernels):
+        cols = [self.shards(k) for k in kernels]
+        n = len(self.ctxs)
+        flat = [cols[j][i].handle if cols[j][i] is not None else None for i in range(n) for j in range(len(cols))]
+        return (_vp * len(flat))(*flat), len(cols)
+
+    def rhs_host(self, kernels, n: np.ndarray, outputs=("p", "q", "s")):
+        n = np.ascontiguousarray(n, dtype=np.float64)
+        res = {name: np.empty(n.size) for name in outputs}
+        arr, nk = self._table(kernels)
+        ptr = lambda name: res[name].ctypes.data if name in res else None  # noqa: E731
+        with self._lock:
+            check(load().ttagg_group_rhs(self.handle, arr, nk, n.ctypes.data, ptr("p"), ptr("q"), ptr("s")),
+                  "ttagg_group_rhs")
+        return res
+
+    def rk2_host(self, kernels, n0: np.ndarray, t0: float, dt: float, steps: int, record_every: int):
+        n = np.array(n0, dtype=np.float64, copy=True)
+        rec = np.zeros((steps // record_every + 1, 5))
+        fail = ctypes.c_int64(0)
+        neg = ctypes.c_int64(0)
+        arr, nk = self._table(kernels)
+        with self._lock:
+            check(load().ttagg_group_rk2(self.handle, arr, nk, n.ctypes.data, float(t0), float(dt), int(steps),
+                                         int(record_every), rec.ctypes.data, ctypes.byref(fail),
+                                         ctypes.byref(neg)), "ttagg_group_rk2")
+        return n, rec, int(fail.value), int(neg.value)
+
+
+_GROUP = None
+_GROUP_ENV_READ = False
+
+
+def set_group(devices) -> "Group | None":
+    """Route rhs_total / integrate through a device group (None: one device)."""
+    global _GROUP, _GROUP_ENV_READ
+    with _LOCK:
+        _GROUP_ENV_READ = True
+        old, _GROUP = _GROUP, (Group(devices) if devices else None)
+    if old is not None:
+        old.close()
+    return _GROUP
+
+
+def active_group() -> "Group | None":
+    """The device group in use ($TTAGG_DEVICES="0,1,..." selects one at first use)."""
+    global _GROUP_ENV_READ
+    if not _GROUP_ENV_READ:
+        with _LOCK:
+            if not _GROUP_ENV_READ:
+                _GROUP_ENV_READ = True
+                env = os.environ.get("TTAGG_DEVICES", "").strip()
+                if env:
+                    globals()["_GROUP"] = Group([int(x) for x in env.split(",") if x.strip()])
+    return _GROUP
 
 
 def get_context(device: int | None = None) -> Context:

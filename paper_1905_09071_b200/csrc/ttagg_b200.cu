@@ -3010,4 +3010,363 @@ int ttagg_profile_read(ttagg_ctx* ctx, double* out72) {
   return TTAGG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Device group: rank-sharded RHS / RK2 over several GPUs of one process
+// (the single-process counterpart of dist.py's torchrun
+// path).  Every device holds its own context and the kernel shards the caller
+// uploaded there; one NCCL all-reduce (sum) per RHS completes dn/dt on every
+// device, which then applies the identical stage update to its replica of n.
+// NCCL is loaded at run time (dlopen, the process's libnccl.so.2 — torch's
+// copy when torch is loaded), so the library has no link-time NCCL
+// dependency and single-device use needs none.
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+  ncclResult_t (*commInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.commInitAll = (decltype(api.commInitAll))dlsym(h, "ncclCommInitAll");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+    api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+    api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
+    api.ok = api.commInitAll && api.commDestroy && api.allReduce && api.groupStart && api.groupEnd && api.errStr;
+  });
+  return api;
+}
+
+#define NCCL_TRY(x)                                                                                 \
+  do {                                                                                              \
+    ncclResult_t r_ = (x);                                                                          \
+    if (r_ != ncclSuccess) return fail(TTAGG_ERR_NCCL, std::string(#x) + ": " + nccl().errStr(r_)); \
+  } while (0)
+
+}  // namespace
+
+struct ttagg_group {
+  int n = 0;
+  std::vector<ttagg_ctx*> ctx;
+  std::vector<cudaStream_t> st;
+  std::vector<ncclComm_t> comm;
+  std::vector<double*> buf;  // per device: natural n, 3 perm states, perm s, 3N natural partials
+  std::vector<size_t> buf_bytes;
+  double* pin = nullptr;  // page-locked staging on device 0's side
+  size_t pin_bytes = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+// all-reduce (sum) of `count` doubles at ptr[i] on every device of the group
+int group_allreduce(ttagg_group* G, const std::vector<double*>& ptr, size_t count) {
+  if (G->n == 1 && G->comm.empty()) return TTAGG_OK;
+  NCCL_TRY(nccl().groupStart());
+  for (int i = 0; i < G->n; ++i) {
+    CUDA_TRY(cudaSetDevice(G->ctx[i]->device));
+    const ncclResult_t r = nccl().allReduce(ptr[i], ptr[i], count, ncclFloat64, ncclSum, G->comm[i], G->st[i]);
+    if (r != ncclSuccess) {
+      nccl().groupEnd();
+      return fail(TTAGG_ERR_NCCL, std::string("ncclAllReduce: ") + nccl().errStr(r));
+    }
+  }
+  NCCL_TRY(nccl().groupEnd());
+  return TTAGG_OK;
+}
+
+int group_kernels(ttagg_group* G, const ttagg_kernel* const* kernels, int nk, int i, std::vector<const ttagg_kernel*>& out,
+                  Geom* g) {
+  out.clear();
+  for (int j = 0; j < nk; ++j) {
+    const ttagg_kernel* k = kernels[(size_t)i * nk + j];
+    if (!k) continue;
+    if (k->ctx != G->ctx[i]) return fail(TTAGG_ERR_ARG, "kernel shard uploaded to another device's context");
+    out.push_back(k);
+  }
+  if (!out.empty()) TRY(check_set(out.data(), (int)out.size(), g));
+  return TTAGG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ttagg_group_create(const int* devices, int n_dev, ttagg_group** out) {
+  if (!devices || !out || n_dev < 1) return fail(TTAGG_ERR_ARG, "a device group needs at least one device");
+  auto* G = new ttagg_group();
+  struct Guard {
+    ttagg_group* g;
+    ~Guard() {
+      if (g) ttagg_group_destroy(g);
+    }
+  } guard{G};
+  G->n = n_dev;
+  for (int i = 0; i < n_dev; ++i) {
+    for (int j = 0; j < i; ++j)
+      if (devices[j] == devices[i]) return fail(TTAGG_ERR_ARG, "a device appears twice in the group");
+    ttagg_ctx* c = nullptr;
+    TRY(ttagg_ctx_create(devices[i], &c));
+    G->ctx.push_back(c);
+    cudaStream_t s = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    G->st.push_back(s);
+    G->buf.push_back(nullptr);
+    G->buf_bytes.push_back(0);
+  }
+  if (n_dev > 1 || getenv("TTAGG_GROUP_NCCL")) {  // one device: no collective needed (forced on for tests)
+    if (!nccl().ok) return fail(TTAGG_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    G->comm.resize(n_dev);
+    NCCL_TRY(nccl().commInitAll(G->comm.data(), n_dev, devices));
+  }
+  *out = G;
+  guard.g = nullptr;
+  return TTAGG_OK;
+}
+
+int ttagg_group_destroy(ttagg_group* G) {
+  if (!G) return TTAGG_OK;
+  for (int i = 0; i < (int)G->ctx.size(); ++i) {
+    cudaSetDevice(G->ctx[i]->device);
+    if (i < (int)G->st.size() && G->st[i]) {
+      cudaStreamSynchronize(G->st[i]);
+      cudaStreamDestroy(G->st[i]);
+    }
+    if (i < (int)G->buf.size()) cudaFree(G->buf[i]);
+  }
+  for (ncclComm_t c : G->comm)
+    if (c) nccl().commDestroy(c);
+  for (ttagg_ctx* c : G->ctx) ttagg_ctx_destroy(c);
+  if (G->pin) cudaFreeHost(G->pin);
+  delete G;
+  return TTAGG_OK;
+}
+
+int ttagg_group_size(const ttagg_group* G, int* n) {
+  if (!G || !n) return fail(TTAGG_ERR_ARG, "null argument");
+  *n = G->n;
+  return TTAGG_OK;
+}
+
+int ttagg_group_ctx(ttagg_group* G, int i, ttagg_ctx** out) {
+  if (!G || !out) return fail(TTAGG_ERR_ARG, "null argument");
+  if (i < 0 || i >= G->n) return fail(TTAGG_ERR_ARG, "device index outside the group");
+  *out = G->ctx[i];
+  return TTAGG_OK;
+}
+
+int ttagg_group_rhs(ttagg_group* G, const ttagg_kernel* const* kernels, int n_kernels, const double* n, double* p,
+                    double* q, double* s) {
+  if (!G || !kernels || !n) return fail(TTAGG_ERR_ARG, "null argument");
+  if (n_kernels < 1) return fail(TTAGG_ERR_EMPTY, "no collision orders configured");
+  std::lock_guard<std::mutex> lock(G->mu);
+  Geom g;
+  bool any = false;
+  std::vector<std::vector<const ttagg_kernel*>> ks(G->n);
+  for (int i = 0; i < G->n; ++i) {
+    Geom gi;
+    TRY(group_kernels(G, kernels, n_kernels, i, ks[i], &gi));
+    if (ks[i].empty()) continue;
+    if (any && gi.N != g.N) return fail(TTAGG_ERR_SIZE, "kernel shards disagree on N");
+    g = gi;
+    any = true;
+  }
+  if (!any) return fail(TTAGG_ERR_EMPTY, "no collision orders configured");
+  for (int64_t j = 0; j < g.N; ++j)  // ConcentrationState's check (rhs.py:71-72)
+    if (!std::isfinite(n[j])) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
+  const int64_t Na = (g.N + 31) & ~(int64_t)31;
+  const size_t nb = (size_t)g.N * sizeof(double);
+  // pinned staging: [n][p][q][s]
+  if (G->pin_bytes < 4 * Na * sizeof(double)) {
+    if (G->pin) cudaFreeHost(G->pin);
+    G->pin = nullptr;
+    G->pin_bytes = 0;
+    CUDA_TRY(cudaHostAlloc((void**)&G->pin, 4 * Na * sizeof(double), cudaHostAllocDefault));
+    G->pin_bytes = 4 * Na * sizeof(double);
+  }
+  par_copy(G->pin, n, nb);
+  std::vector<double*> part(G->n);
+  for (int i = 0; i < G->n; ++i) {
+    ttagg_ctx* c = G->ctx[i];
+    CUDA_TRY(cudaSetDevice(c->device));
+    const size_t need = (size_t)4 * Na * sizeof(double);
+    if (G->buf_bytes[i] < need) {
+      cudaFree(G->buf[i]);
+      G->buf[i] = nullptr;
+      G->buf_bytes[i] = 0;
+      CUDA_TRY(cudaMalloc(&G->buf[i], need));
+      G->buf_bytes[i] = need;
+    }
+    double* nd = G->buf[i];
+    part[i] = nd + Na;  // [p][q][s], contiguous: one all-reduce
+    if (ks[i].empty()) {
+      CUDA_TRY(cudaMemsetAsync(part[i], 0, 3 * Na * sizeof(double), G->st[i]));
+      continue;
+    }
+    CUDA_TRY(cudaMemcpyAsync(nd, G->pin, nb, cudaMemcpyHostToDevice, G->st[i]));
+    TRY(ttagg_rhs(c, ks[i].data(), (int)ks[i].size(), nd, part[i], part[i] + Na, part[i] + 2 * Na,
+                  TTAGG_WANT_P | TTAGG_WANT_Q, G->st[i]));
+  }
+  TRY(group_allreduce(G, part, 3 * (size_t)Na));
+  CUDA_TRY(cudaSetDevice(G->ctx[0]->device));
+  CUDA_TRY(cudaMemcpyAsync(G->pin + Na, part[0], 3 * Na * sizeof(double), cudaMemcpyDeviceToHost, G->st[0]));
+  for (int i = 0; i < G->n; ++i) {
+    CUDA_TRY(cudaSetDevice(G->ctx[i]->device));
+    CUDA_TRY(cudaStreamSynchronize(G->st[i]));
+  }
+  double* outs[3] = {p, q, s};
+  for (int j = 0; j < 3; ++j)
+    if (outs[j]) par_copy(outs[j], G->pin + (size_t)(j + 1) * Na, nb);
+  return TTAGG_OK;
+}
+
+int ttagg_group_rk2(ttagg_group* G, const ttagg_kernel* const* kernels, int n_kernels, double* n_inout, double t0,
+                    double dt, int64_t steps, int64_t record_every, double* records, int64_t* fail_step,
+                    int64_t* neg_step) {
+  if (!G || !kernels || !n_inout || !records || !fail_step || !neg_step) return fail(TTAGG_ERR_ARG, "null argument");
+  if (!(dt > 0)) return fail(TTAGG_ERR_ARG, "dt must be positive");
+  if (steps < 1 || record_every < 1) return fail(TTAGG_ERR_ARG, "steps and record_every must be >= 1");
+  if (n_kernels < 1) return fail(TTAGG_ERR_EMPTY, "no collision orders configured");
+  std::lock_guard<std::mutex> lock(G->mu);
+  Geom g;
+  bool any = false;
+  std::vector<std::vector<const ttagg_kernel*>> ks(G->n);
+  for (int i = 0; i < G->n; ++i) {
+    Geom gi;
+    TRY(group_kernels(G, kernels, n_kernels, i, ks[i], &gi));
+    if (ks[i].empty()) continue;
+    if (any && gi.N != g.N) return fail(TTAGG_ERR_SIZE, "kernel shards disagree on N");
+    g = gi;
+    any = true;
+  }
+  if (!any) return fail(TTAGG_ERR_EMPTY, "no collision orders configured");
+  for (int64_t j = 0; j < g.N; ++j)
+    if (!std::isfinite(n_inout[j])) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
+  const int64_t nrows = steps / record_every + 1;
+  const int64_t Na = (g.N + 31) & ~(int64_t)31;
+  const size_t nb = (size_t)g.N * sizeof(double);
+  const int nblk = (int)((g.Np + 255) / 256);
+  // per device: [nat Na][A Np][B Np][C Np][s Np]; device 0 also [rec nrows*4]
+  std::vector<double*> vA(G->n), vB(G->n), vC(G->n), vS(G->n);
+  for (int i = 0; i < G->n; ++i) {
+    ttagg_ctx* c = G->ctx[i];
+    CUDA_TRY(cudaSetDevice(c->device));
+    const size_t need = (size_t)(Na + 4 * g.Np + (i == 0 ? nrows * 4 : 0)) * sizeof(double) + 1024;
+    if (G->buf_bytes[i] < need) {
+      cudaFree(G->buf[i]);
+      G->buf[i] = nullptr;
+      G->buf_bytes[i] = 0;
+      CUDA_TRY(cudaMalloc(&G->buf[i], need));
+      G->buf_bytes[i] = need;
+    }
+    double* nat = G->buf[i];
+    vA[i] = nat + Na;
+    vB[i] = vA[i] + g.Np;
+    vC[i] = vB[i] + g.Np;
+    vS[i] = vC[i] + g.Np;
+    CUDA_TRY(cudaMemcpyAsync(nat, n_inout, nb, cudaMemcpyHostToDevice, G->st[i]));
+    TRY(launch_permute(nat, vA[i], g, 0, G->st[i]));
+  }
+  ttagg_ctx* c0 = G->ctx[0];
+  cudaStream_t s0 = G->st[0];
+  double* rec = vS[0] + g.Np;
+  CUDA_TRY(cudaSetDevice(c0->device));
+  TRY(ensure((void**)&c0->diagp, &c0->diagp_bytes, (size_t)2 * nblk * DIAGW * sizeof(double)));
+  double* dpm = c0->diagp;
+  double* dpn = c0->diagp + (size_t)nblk * DIAGW;
+  double* dmid = c0->diag;
+  double* dnew = c0->diag + DIAGW;
+  double* d0 = c0->diag + 2 * DIAGW;
+  stage_kernel<<<nblk, 256, 0, s0>>>(vA[0], vA[0], 0.0, nullptr, g.N, g.N1, g.N2, dpn);
+  diag_finalize_kernel<<<1, 256, 0, s0>>>(dpn, nblk, d0);
+  rk2_book_init_kernel<<<1, 32, 0, s0>>>(d0, c0->book, rec);
+  CUDA_TRY(cudaGetLastError());
+  // partial RHS at x (perm) into vS on every device, then the all-reduce
+  auto rhs = [&](const std::vector<double*>& x) -> int {
+    for (int i = 0; i < G->n; ++i) {
+      ttagg_ctx* c = G->ctx[i];
+      CUDA_TRY(cudaSetDevice(c->device));
+      if (ks[i].empty()) {
+        CUDA_TRY(cudaMemsetAsync(vS[i], 0, g.Np * sizeof(double), G->st[i]));
+        continue;
+      }
+      TRY(ttagg_rhs_perm(c, ks[i].data(), (int)ks[i].size(), x[i], nullptr, 0.0, vS[i], G->st[i]));
+    }
+    return group_allreduce(G, vS, (size_t)g.Np);
+  };
+  // out = base + a s on every device; diagnostics on device 0
+  auto stage = [&](const std::vector<double*>& base, double a, const std::vector<double*>& out, double* dp,
+                   double* dg) -> int {
+    for (int i = 0; i < G->n; ++i) {
+      CUDA_TRY(cudaSetDevice(G->ctx[i]->device));
+      stage_kernel<<<nblk, 256, 0, G->st[i]>>>(base[i], vS[i], a, out[i], g.N, g.N1, g.N2, i == 0 ? dp : nullptr);
+      if (i == 0) diag_finalize_kernel<<<1, 256, 0, G->st[i]>>>(dp, nblk, dg);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return TTAGG_OK;
+  };
+  std::vector<double*> cur = vA, mid = vB, nxt = vC;
+  int64_t host_book[4] = {0, 0, 0, 0};
+  for (int64_t step = 1; step <= steps; ++step) {
+    TRY(rhs(cur));
+    TRY(stage(cur, 0.5 * dt, mid, dpm, dmid));
+    TRY(rhs(mid));
+    TRY(stage(cur, dt, nxt, dpn, dnew));
+    CUDA_TRY(cudaSetDevice(c0->device));
+    rk2_book_kernel<<<1, 32, 0, s0>>>(dmid, dnew, c0->book, record_every, rec);
+    CUDA_TRY(cudaGetLastError());
+    std::swap(cur, nxt);
+    if (step % 64 == 0 || step == steps) {
+      CUDA_TRY(cudaMemcpyAsync(host_book, c0->book, sizeof(host_book), cudaMemcpyDeviceToHost, s0));
+      CUDA_TRY(cudaStreamSynchronize(s0));
+      if (host_book[1] != 0) break;
+    }
+  }
+  CUDA_TRY(cudaSetDevice(c0->device));
+  CUDA_TRY(cudaMemcpyAsync(host_book, c0->book, sizeof(host_book), cudaMemcpyDeviceToHost, s0));
+  TRY(launch_permute(cur[0], G->buf[0], g, 1, s0));
+  std::vector<double> hrec((size_t)nrows * 4);
+  CUDA_TRY(cudaMemcpyAsync(hrec.data(), rec, hrec.size() * sizeof(double), cudaMemcpyDeviceToHost, s0));
+  CUDA_TRY(cudaMemcpyAsync(n_inout, G->buf[0], nb, cudaMemcpyDeviceToHost, s0));
+  for (int i = 0; i < G->n; ++i) {
+    CUDA_TRY(cudaSetDevice(G->ctx[i]->device));
+    CUDA_TRY(cudaStreamSynchronize(G->st[i]));
+  }
+  const int64_t rows = std::min<int64_t>(host_book[3], nrows);
+  std::vector<double> outr((size_t)nrows * 5, 0.0);
+  double t = t0;
+  int64_t row = 0;
+  for (int64_t stp = 0; row < rows; ++stp) {
+    if (stp > 0) t = t + dt;
+    if (stp % record_every == 0) {
+      outr[row * 5] = t;
+      for (int cc = 0; cc < 4; ++cc) outr[row * 5 + 1 + cc] = hrec[row * 4 + cc];
+      ++row;
+    }
+  }
+  std::memcpy(records, outr.data(), outr.size() * sizeof(double));
+  *fail_step = host_book[1];
+  *neg_step = host_book[2];
+  return TTAGG_OK;
+}
+
 }  // extern "C"

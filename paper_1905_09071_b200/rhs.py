@@ -24,7 +24,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import get_context
+from ._lib import active_group, get_context
 from .kernels import CPKernel, DenseKernel, KernelError, TTKernel
 from .parallel import SERIAL_PLAN, ExecutionPlan
 
@@ -209,6 +209,10 @@ def _one(kernel, state, want_p: bool, want_q: bool, kind_ok, label: str):
     d, n = _check_pair(kernel, state)
     if kind_ok is _is_dense:
         _dense_budget_check(d, n.size)
+    grp = active_group()
+    if grp is not None:
+        out = grp.rhs_host([kernel], n, outputs=("p",) if want_p else ("q",))
+        return out["p"] if want_p else out["q"]
     ctx = get_context()
     dk = ctx.device_kernel(kernel)
     out = ctx.rhs_host([dk], n, want_p=want_p, want_q=want_q,
@@ -285,16 +289,22 @@ def rhs_total(kernels: KernelSet, state: ConcentrationState, plan: ExecutionPlan
             raise KernelError(f"unsupported kernel representation {type(k).__name__}")
         if _is_dense(k):
             _dense_budget_check(d, n.size)
-    ctx = get_context()
-    dks = [ctx.device_kernel(k) for _, k in items]
+    grp = active_group()
+    if grp is not None:  # several GPUs: rank-sharded partials, one all-reduce
+        run = lambda objs, outputs=("p", "q", "s"): grp.rhs_host(objs, n, outputs=outputs)  # noqa: E731
+        units = [k for _, k in items]
+    else:
+        ctx = get_context()
+        run = lambda dks, outputs=("p", "q", "s"): ctx.rhs_host(dks, n, outputs=outputs)  # noqa: E731
+        units = [ctx.device_kernel(k) for _, k in items]
     if not breakdown:
-        out = ctx.rhs_host(dks, n)
+        out = run(units)
         return RhsResult(p=out["p"], q=out["q"], s=out["s"], by_order=None)
     p = np.zeros(n.size)
     q = np.zeros(n.size)
     per = {}
-    for (d, _), dk in zip(items, dks):
-        out = ctx.rhs_host([dk], n, outputs=("p", "q"))
+    for (d, _), u in zip(items, units):
+        out = run([u], outputs=("p", "q"))
         p += out["p"]
         q += out["q"]
         per[d] = (out["p"], out["q"])
