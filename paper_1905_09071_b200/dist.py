@@ -96,15 +96,28 @@ class CudaEngine:
         else:
             out.zero_()
 
-    def stage(self, base, s, a, out, slot=0):
+    def stage(self, base, s, a, out, slot=0, row=None):
         """out = base + a s; diagnostics (nonfinite, min, max|.|, M0, M1, M2)
-        stay on the device in `slot` until :meth:`diags` reads them."""
+        stay on the device — in `slot` of :meth:`diags`, or in row `row` of
+        the history (:meth:`diag_history`) — until read."""
+        d = self.diag[slot] if row is None else self.hist[row, slot]
         self.ctx.stage(self.n_classes, base.data_ptr(), s.data_ptr(), a,
-                       None if out is None else out.data_ptr(), self.diag[slot].data_ptr(), self._stream())
+                       None if out is None else out.data_ptr(), d.data_ptr(), self._stream())
 
     def diags(self) -> np.ndarray:
         """Both diagnostic slots in one device-to-host read: (2, 6)."""
         return self.diag.cpu().numpy()[:, :6]
+
+    def diag_history(self, rows: int):
+        """Device rows for the diagnostics of `rows` steps (2 stages each)."""
+        self.hist = self.torch.zeros((rows, 2, 8), dtype=self.torch.float64, device=self.device)
+
+    def read_history(self, rows: int) -> np.ndarray:
+        """The first `rows` history rows in one device-to-host read: (rows, 2, 6)."""
+        return self.hist[:rows].cpu().numpy()[:, :, :6]
+
+    def copy(self, v):
+        return v.clone()
 
 
 @dataclass
@@ -135,9 +148,16 @@ class DistRHS:
         self.engine.partial(n, k, alpha, out)
         return self.allreduce(out)
 
-    def rk2(self, n0: np.ndarray, t0: float, dt: float, steps: int, record_every: int = 1) -> DistRK2Result:
+    def rk2(self, n0: np.ndarray, t0: float, dt: float, steps: int, record_every: int = 1,
+            poll_every: int = 64) -> DistRK2Result:
         """Explicit midpoint (integrator.py:153-228) with the state resident on the device:
-        k1 = S(n); mid = n + dt/2 k1; k2 = S(mid); n <- n + dt k2 (all-reduce per S)."""
+        k1 = S(n); mid = n + dt/2 k1; k2 = S(mid); n <- n + dt k2 (all-reduce per S).
+
+        The stage diagnostics of each step stay on the device and are read
+        once every `poll_every` steps (one host sync per chunk, not per
+        step); a failing step found in a chunk is re-located by replaying the
+        chunk from its saved first state, so the returned state is the last
+        finite one, as in the per-step loop."""
         if not dt > 0:
             raise ValueError("dt must be positive")
         e = self.engine
@@ -150,22 +170,42 @@ class DistRHS:
         d0 = e.diags()[0]  # diagnostics of the initial state
         res = DistRK2Result(n=np.asarray(n0))
         res.rows.append((float(t0), float(d0[3]), float(d0[4]), float(d0[5]), float(d0[1])))
-        t = float(t0)
-        for step in range(1, steps + 1):
+        K = max(1, min(poll_every, steps))
+        e.diag_history(K)
+
+        def one_step(row):
+            nonlocal n, nxt
             self.rhs(n, out=s)
-            e.stage(n, s, 0.5 * dt, mid, 0)
+            e.stage(n, s, 0.5 * dt, mid, 0, row)
             self.rhs(mid, out=s)
-            e.stage(n, s, dt, nxt, 1)
-            dm, dn = e.diags()  # one host sync per step
-            if dm[0] != 0.0 or dn[0] != 0.0:
-                res.fail_step = step
-                break
+            e.stage(n, s, dt, nxt, 1, row)
             n, nxt = nxt, n
-            t = t + dt
-            if res.neg_step == 0 and dn[1] < -1e-9 * dn[2]:
-                res.neg_step = step
-            if step % record_every == 0:
-                res.rows.append((t, float(dn[3]), float(dn[4]), float(dn[5]), float(dn[1])))
+
+        t = float(t0)
+        step = 0
+        while step < steps:
+            first = e.copy(n)
+            count = min(K, steps - step)
+            for j in range(count):
+                one_step(j)
+            hist = e.read_history(count)  # one host sync per chunk
+            for j in range(count):
+                dm, dn = hist[j]
+                stp = step + j + 1
+                if dm[0] != 0.0 or dn[0] != 0.0:
+                    res.fail_step = stp
+                    n = first  # replay up to the last finite state
+                    for jj in range(j):
+                        one_step(jj)
+                    break
+                t = t + dt
+                if res.neg_step == 0 and dn[1] < -1e-9 * dn[2]:
+                    res.neg_step = stp
+                if stp % record_every == 0:
+                    res.rows.append((t, float(dn[3]), float(dn[4]), float(dn[5]), float(dn[1])))
+            if res.fail_step:
+                break
+            step += count
         res.n = e.from_layout(n)
         return res
 

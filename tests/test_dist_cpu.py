@@ -51,16 +51,29 @@ class OracleEngine:
             acc += orc.tt_loss(self.tt[d], x)
         out.copy_(torch.from_numpy(acc))
 
-    def stage(self, base, s, a, out, slot=0):
+    def stage(self, base, s, a, out, slot=0, row=None):
         v = (base + a * s).numpy()
         k = np.arange(1, v.size + 1, dtype=np.float64)
         if out is not None:
             out.copy_(torch.from_numpy(v))
-        self._diag[slot] = np.array([0.0 if np.all(np.isfinite(v)) else 1.0, v.min(), np.abs(v).max(),
-                                     v.sum(), k @ v, (k * k) @ v])
+        d = np.array([0.0 if np.all(np.isfinite(v)) else 1.0, v.min(), np.abs(v).max(),
+                      v.sum(), k @ v, (k * k) @ v])
+        if row is None:
+            self._diag[slot] = d
+        else:
+            self._hist[row, slot] = d
 
     def diags(self):
         return self._diag.copy()
+
+    def diag_history(self, rows):
+        self._hist = np.zeros((rows, 2, 6))
+
+    def read_history(self, rows):
+        return self._hist[:rows].copy()
+
+    def copy(self, v):
+        return v.clone()
 
 
 def _free_port():
@@ -195,3 +208,35 @@ def test_world2_tt_rank_sharding_matches_unsharded_oracle():
     for _, s, n in out:
         assert rel_inf(s, s_ref) <= 1e-12
         assert rel_inf(n, n_ref) <= 1e-12
+
+
+def test_chunked_diagnostics_polling_matches_per_step_semantics():
+    """DistRHS.rk2 reads the stage diagnostics once per chunk: chunk
+    boundaries change nothing, and a failing step inside a chunk is reported
+    at the reference's step with the last finite state (oracle integrate,
+    integrator.py:207-215)."""
+    N = 120
+    exps = (0.1, -0.1, 0.05)
+    f = {d: permutation_power_cp(exps[:d], N) for d in (2, 3)}
+    shard = lpt_rank_shards(rank_counts_of(f), 1)[0]
+    n0 = np.exp(-np.arange(1, N + 1) / 15.0)
+    n0 = n0 / n0.sum()
+    drhs = DistRHS(OracleEngine(f, shard, N))
+    a = drhs.rk2(n0, 0.0, 0.01, 10, record_every=2, poll_every=3)
+    b = drhs.rk2(n0, 0.0, 0.01, 10, record_every=2, poll_every=64)
+    np.testing.assert_array_equal(a.n, b.n)
+    assert a.rows == b.rows and a.fail_step == b.fail_step == 0
+    kern = {d: {"kind": "cp", "arrays": f[d]} for d in f}
+    ref_n, _, _ = orc.integrate(kern, n0, dt=0.01, steps=10)
+    assert rel_inf(a.n, ref_n) <= 1e-12
+    # a step size that blows up: the oracle raises at some step k
+    big = 400.0
+    with pytest.raises(orc.OracleStepFailure) as exc:
+        orc.integrate(kern, n0, dt=big, steps=40)
+    k = exc.value.step_index
+    for poll in (1, 3, 64):
+        r = drhs.rk2(n0, 0.0, big, 40, poll_every=poll)
+        assert r.fail_step == k
+        if k > 1:
+            ref_last, _, _ = orc.integrate(kern, n0, dt=big, steps=k - 1)
+            assert rel_inf(r.n, ref_last) <= 1e-12
