@@ -40,13 +40,21 @@ def grid_count(g):
 
 def label(rows):
     """[(kernel, grid, value...)] in issue order -> labels 'passA d=5' etc.
-    qcoef launches (fill stream) belong to the oldest pass A whose qcoef has
-    not been seen yet; pass C follows its own order's pass B."""
+    Pass A: the grid gives the order for the one-CTA-per-item kernels
+    (npairs x N2 CTAs); the persistent TMA-fed pass A launches a fixed grid,
+    so its launches are labelled by issue order (cheapest order first, the
+    costliest last: run_orders).  qcoef launches belong to the oldest pass A
+    whose qcoef has not been seen yet; pass C follows its own order's pass B."""
     out, cur, pending = [], None, []
+    a_order = sorted(C5_PAIRS.values())
+    na = 0
     for name, grid in rows:
         k = short(name)
         if k.startswith("passA"):
-            cur = C5_PAIRS.get(grid // N2)
+            cur = C5_PAIRS.get(grid // N2) if k.startswith("passA_big") or k.startswith("passA_kernel") else None
+            if cur is None:
+                cur = a_order[min(na, len(a_order) - 1)]
+            na += 1
             pending.append(cur)
             out.append(f"passA d={cur}")
         elif k.startswith("passB"):
@@ -72,8 +80,7 @@ def launches(path, tag, command):
     segs = []  # complete C5 RHS evaluations (the order-5 pass A has 300 pairs x N2 CTAs)
     for a in starts:
         b = next((e for e in ends if e > a), None)
-        if b is not None and any(names[i].startswith("passA") and grid_count(rows[i]["Grid Size"]) == 300 * N2
-                                 for i in range(a, b)):
+        if b is not None and sum(names[i].startswith("passA") for i in range(a, b)) == len(C5_PAIRS):
             segs.append((a, b))
     a, b = segs[-1]
     seg = rows[a: b + 1]
