@@ -298,19 +298,22 @@ __device__ __forceinline__ void emit_pm(const PassAArgs& a, const PMOut& o, int 
 // conj(w) cn2 = conj(b) PMst[r] (PMst[r] = conj(Pst[r]) cn2): two complex
 // multiplies per output instead of three.  Assumes res_cnt[0] = N1/2 + 1 and
 // res_cnt[j>0] = N1/2 (checked on the host).
+// rbase: the residues' first exchange rows (res_base, staged in shared memory
+// by the caller: a dynamically indexed kernel-parameter array costs constant-
+// cache round trips)
 template <int N1>
-__device__ __forceinline__ void emit_split(const PassAArgs& a, const PMOut& o, int d, int j, int t, const cplx (&v)[16],
+__device__ __forceinline__ void emit_split(const int* rbase, const PMOut& o, int d, int j, int t, const cplx (&v)[16],
                                            cplx b, const double2* Pst, const double2* PMst) {
   constexpr int T = N1 / 16;
-  double2* TP = o.TP + a.res_base[j];
+  double2* TP = o.TP + rbase[j];
 #pragma unroll
   for (int r = 0; r < 8; ++r) sts_c(TP + t + T * r, cmul(v[r], cmul(b, lds_c(Pst + r))));
   const cplx bc = cconj(b);
-  double2* TM = j == 0 ? o.TM + a.res_base[0] + N1 - t : o.TM + a.res_base[d - j] + (N1 - 1 - t);
+  double2* TM = j == 0 ? o.TM + rbase[0] + N1 - t : o.TM + rbase[d - j] + (N1 - 1 - t);
 #pragma unroll
   for (int r = 8; r < 16; ++r) sts_c(TM - T * r, cmul(cconj(v[r]), cmul(bc, lds_c(PMst + r))));
   if (t == 0 && j == 0) {
-    sts_c(o.TM + a.res_base[0], cconj(v[0]));
+    sts_c(o.TM + rbase[0], cconj(v[0]));
     sts_c(TP + T * 8, cmul(v[8], cmul(b, lds_c(Pst + 8))));
   }
 }
@@ -527,6 +530,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
   __shared__ double2 Pst[2][16], PMst[2][16];
   __shared__ double2 Ust[2][MAXRES];
   __shared__ double2 Kst[MAXRES][16];
+  __shared__ int rbase[MAXRES];
   __shared__ __align__(8) uint64_t mbar;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int d = a.d;
@@ -539,6 +543,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
     const cplx w = ld_c(a.tabK + (j * T * r) % K);
     Kst[j][r] = make_double2(w.x, w.y);
   }
+  if (t < MAXRES) rbase[t] = a.res_base[t];
   fft_stage_table<N1>(stw, a.tw, t, T);
   auto issue = [&](int it) {  // one thread: bulk-copy item it's row into zs
     const int pair = a.pair0 + it / N2, n2 = it % N2;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
     }
     // residue 0 straight from the registers
     fft_fwd_split<N1>(z, t, ex, a.tw, CtaSync(), stw);
-    emit_split<N1>(a, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
+    emit_split<N1>(rbase, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
     for (int j = 1; j < d; ++j) {
       cplx v[E];
       const cplx tb = ld_c(a.tabK + j * t);
@@ -638,7 +643,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
         if (t == 0 && next < nitems) issue(next);
       }
       fft_fwd_split<N1>(v, t, ex, a.tw, CtaSync(), stw);
-      emit_split<N1>(a, o, d, j, t, v, cmul(ct, lds_c(&Ust[pb][j])), Pst[pb], PMst[pb]);
+      emit_split<N1>(rbase, o, d, j, t, v, cmul(ct, lds_c(&Ust[pb][j])), Pst[pb], PMst[pb]);
     }
   }
 }
