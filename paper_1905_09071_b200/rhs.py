@@ -50,6 +50,25 @@ _SYMMETRY_CHECK_MAX_N = 64
 _SYMMETRY_TOL = 1e-8
 
 
+_PIN_MIN = 1 << 16
+
+
+def _host_copy(n: np.ndarray) -> np.ndarray:
+    """The state's own copy (rhs.py:66-68); large states land in page-locked
+    memory so every RHS on them transfers by DMA without a staging copy."""
+    if n.size >= _PIN_MIN:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                out = torch.empty(n.size, dtype=torch.float64, pin_memory=True).numpy()
+                np.copyto(out, n)
+                return out
+        except Exception:  # no CUDA runtime: plain copy
+            pass
+    return n.copy()
+
+
 @dataclass(frozen=True)
 class ConcentrationState:
     """Per-size concentrations n_1..n_N at time t (rhs.py:54-79)."""
@@ -59,8 +78,8 @@ class ConcentrationState:
 
     def __post_init__(self):
         n = np.ascontiguousarray(self.n, dtype=np.float64)
-        if n is self.n:
-            n = n.copy()
+        if n is self.n or n.size >= _PIN_MIN:
+            n = _host_copy(n)
         if n.ndim != 1 or n.size < 2:
             raise ValueError("concentration state must be a vector of length >= 2")
         if not np.all(np.isfinite(n)):
