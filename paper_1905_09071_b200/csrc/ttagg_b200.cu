@@ -205,6 +205,7 @@ struct ttagg_kernel {
   int* fdesc = nullptr;  // TT: descriptors of the uploaded (live) fibers
   int* cidx = nullptr;   // TT: full fiber index -> uploaded column or -1
   int C_full = 0;        // TT: fibers before dropping
+  int live_cols = 0;     // TT: uploaded live fibers (C less the no-op alignment slots)
   double* dots = nullptr;
   double* coef = nullptr;
   OrderPlan* plan = nullptr;
@@ -648,6 +649,26 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
   }
 }
 
+// ---- tensor memory (TMEM) as per-thread storage (tcgen05.alloc / st / ld):
+// 16 complex values <-> 64 TMEM columns of the thread's lane (32x32b shape:
+// warp w of a 4-warp CTA owns lanes 32w..32w+31)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
 // ---------------------------------------------------------------------------
 // pass B: row FFTs, spectral product / chain, inverse row FFTs
 // ---------------------------------------------------------------------------
@@ -673,6 +694,10 @@ struct PassBArgs {
 // core-major, rn-major, rp-inner order; first/last mark the first and last
 // live fiber that feeds chain state (core, rn).
 constexpr int FD_FIRST = 1 << 20, FD_LAST = 1 << 21, FD_NOOP = 1 << 22;
+// the column accumulates into the chain's second accumulator (tensor memory):
+// cores with several output states pair their fibers by output state (rn, rn+1)
+// at the same input state rp, so both halves of a pair read one chain state
+constexpr int FD_ACC1 = 1 << 23;
 __host__ __device__ constexpr int fd_pack(int lam, int rn, int rp, bool first, bool last) {
   return lam | (rn << 4) | (rp << 12) | (first ? FD_FIRST : 0) | (last ? FD_LAST : 0);
 }
@@ -707,7 +732,18 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
   static_assert(!TMA || (N2 == 256 && ROWS == 8 && STG % 8 == 0), "TMA staging: 8 rows x 256, 128-byte aligned");
   extern __shared__ __align__(128) double2 smem[];
   __shared__ __align__(8) uint64_t mbar;  // TMA: both planes of the next pair landed
+  __shared__ uint32_t tm_base;            // TT: the second chain accumulator (64 TMEM columns)
   unsigned parity = 0;
+  if constexpr (TT) {
+    if ((threadIdx.x >> 5) == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&tm_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       mbar_init(&mbar, 1);
@@ -726,6 +762,7 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
   const int C = a.C;
   // TT: per-CTA chain scratch (reused by every row block of this CTA)
   const size_t slot = (size_t)blockIdx.x * 2 * a.Rmax;
+  const uint32_t tacc = TT ? tm_base + ((uint32_t)(32 * (tid >> 5)) << 16) : 0u;
   auto st = [&](int b, int r, int i) -> double2* {
     return a.scratch + ((slot + (size_t)b * a.Rmax + r) * E + i) * blockDim.x + tid;
   };
@@ -797,6 +834,36 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
         if (lam == 0) {
 #pragma unroll
           for (int i = 0; i < E; ++i) sts_c(st(0, rn, i), X[i]);
+        } else if (f & FD_ACC1) {
+          // second accumulator: four values at a time through tensor memory
+          // (rn-paired cores are never the last core, so a finished state
+          // always goes to the chain scratch)
+#pragma unroll
+          for (int q = 0; q < E / 4; ++q) {
+            uint32_t r[16];
+            if (!(f & FD_FIRST)) {
+              tmem_ld16(tacc + 16 * q, r);
+              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = 4 * q + u;
+              cplx v = (f & FD_FIRST) ? mk(0.0, 0.0)
+                                      : mk(__hiloint2double((int)r[4 * u + 1], (int)r[4 * u]),
+                                           __hiloint2double((int)r[4 * u + 3], (int)r[4 * u + 2]));
+              v = cadd(v, cmul(from_sb ? lds_c(Sb + i * 128 + tid) : lds_c(st((lam - 1) & 1, rp, i)), X[i]));
+              if (f & FD_LAST) {
+                sts_c(st(lam & 1, rn, i), v);
+              } else {
+                r[4 * u + 0] = (uint32_t)__double2loint(v.x);
+                r[4 * u + 1] = (uint32_t)__double2hiint(v.x);
+                r[4 * u + 2] = (uint32_t)__double2loint(v.y);
+                r[4 * u + 3] = (uint32_t)__double2hiint(v.y);
+              }
+            }
+            if (!(f & FD_LAST)) tmem_st16(tacc + 16 * q, r);
+          }
+          if (!(f & FD_LAST)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         } else {
           if (f & FD_FIRST) {
 #pragma unroll
@@ -884,8 +951,15 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
         vp[i] = cadd(P, vm[i]);
         vm[i] = mul_mi(csub(P, vm[i]));
       }
+      bool pre1 = false;  // TT: the pair's second fiber reads the same (prefetched) chain state
+      if constexpr (TT) {
+        if (pre && 2 * p + 1 < C) {
+          const int f0 = __ldg(a.fdesc + 2 * p), f1 = __ldg(a.fdesc + 2 * p + 1);
+          pre1 = !(f1 & FD_NOOP) && fd_lam(f1) == fd_lam(f0) && fd_rp(f1) == fd_rp(f0);
+        }
+      }
       process(vp, 2 * p, pre);
-      if (2 * p + 1 < C) process(vm, 2 * p + 1, false);
+      if (2 * p + 1 < C) process(vm, 2 * p + 1, pre1);
       pre = false;
     }
     cp_async_wait<0>();
@@ -912,6 +986,12 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
         sts_c(a.U + (size_t)n2 * a.K_rows + rho, u);
       }
     }
+  }
+  if constexpr (TT) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tm_base) : "memory");
   }
 }
 
@@ -2536,21 +2616,61 @@ int ttagg_tt_upload(ttagg_ctx* ctx, int d, int64_t n_classes, const int64_t* ran
           if (f) used[l][rp] = 1;
         }
   }
+  // Column order: core-major.  The first core and the last one (a single
+  // input or output state) list their live fibers rn-major, rp-inner.  Every
+  // other core pairs its output states (rn, rn+1): for each rp the two fibers
+  // (rp, rn) and (rp, rn+1) share one exchange pair and one read of the chain
+  // state rp — half the state traffic of rp-inner pairs — the second one
+  // accumulating in the pass-B CTA's tensor memory (FD_ACC1); a dropped fiber
+  // keeps its slot as a no-op, and an odd last output state falls back to
+  // rp-inner pairs.
   std::vector<int> cidx(C, -1), desc;
-  for (int l = 0; l < d; ++l)
-    for (int rn = 0; rn < k->ranks[l + 1]; ++rn) {
-      int first = -1, last = -1;
-      for (int rp = 0; rp < k->ranks[l]; ++rp)
-        if (live[fidx(l, rp, rn)]) {
-          if (first < 0) first = rp;
-          last = rp;
-        }
-      for (int rp = 0; rp < k->ranks[l]; ++rp)
-        if (live[fidx(l, rp, rn)]) {
-          cidx[fidx(l, rp, rn)] = (int)desc.size();
-          desc.push_back(fd_pack(l, rn, rp, rp == first, rp == last));
-        }
+  auto group_ends = [&](int l, int rn, int& first, int& last) {
+    first = last = -1;
+    for (int rp = 0; rp < k->ranks[l]; ++rp)
+      if (live[fidx(l, rp, rn)]) {
+        if (first < 0) first = rp;
+        last = rp;
+      }
+  };
+  auto push = [&](int l, int rp, int rn, int extra) {
+    int first, last;
+    group_ends(l, rn, first, last);
+    cidx[fidx(l, rp, rn)] = (int)desc.size();
+    desc.push_back(fd_pack(l, rn, rp, rp == first, rp == last) | extra);
+  };
+  for (int l = 0; l < d; ++l) {
+    const int rp_n = k->ranks[l], rn_n = k->ranks[l + 1];
+    bool paired = l > 0 && l < d - 1 && rn_n >= 2 && rp_n >= 2;
+    if (paired) {  // only where the no-op slots stay rare (dense cores): they cost column transforms
+      int live_n = 0, slots = 0;
+      for (int rn = 0; rn < rn_n; ++rn)
+        for (int rp = 0; rp < rp_n; ++rp) live_n += live[fidx(l, rp, rn)];
+      for (int rn = 0; rn + 1 < rn_n; rn += 2)
+        for (int rp = 0; rp < rp_n; ++rp) slots += 2 * (live[fidx(l, rp, rn)] || live[fidx(l, rp, rn + 1)]);
+      for (int rp = 0; rp < rp_n && (rn_n & 1); ++rp) slots += live[fidx(l, rp, rn_n - 1)];
+      paired = slots * 20 <= live_n * 21;  // <= 5% no-ops
     }
+    int rn = 0;
+    if (paired) {
+      for (; rn + 1 < rn_n; rn += 2) {
+        bool any = false;
+        for (int rp = 0; rp < rp_n && !any; ++rp) any = live[fidx(l, rp, rn)] || live[fidx(l, rp, rn + 1)];
+        if (!any) continue;
+        if (desc.size() & 1) desc.push_back(FD_NOOP);  // pairs start on an even column
+        for (int rp = 0; rp < rp_n; ++rp) {
+          const bool a0 = live[fidx(l, rp, rn)], a1 = live[fidx(l, rp, rn + 1)];
+          if (!a0 && !a1) continue;
+          if (a0) push(l, rp, rn, 0); else desc.push_back(FD_NOOP);
+          if (a1) push(l, rp, rn + 1, FD_ACC1); else desc.push_back(FD_NOOP);
+        }
+      }
+    }
+    for (; rn < rn_n; ++rn)
+      for (int rp = 0; rp < rp_n; ++rp)
+        if (live[fidx(l, rp, rn)]) push(l, rp, rn, 0);
+  }
+  for (int f : desc) k->live_cols += !(f & FD_NOOP);
   if (desc.empty()) desc.push_back(FD_NOOP);  // an all-zero kernel: one zero column
   k->C = (int)desc.size();
   k->C_pad = (k->C + 1) & ~1;
@@ -2666,7 +2786,7 @@ int ttagg_kernel_info(const ttagg_kernel* k, int64_t* info) {
   info[0] = k->kind;
   info[1] = k->d;
   info[2] = k->N;
-  info[3] = k->C;
+  info[3] = k->kind == TTAGG_KIND_TT ? k->live_cols : k->C;
   info[4] = k->g.Np;
   info[5] = k->g.N1;
   info[6] = k->g.N2;
