@@ -480,7 +480,10 @@ class Group:
 
     def rhs_host(self, kernels, n: np.ndarray, outputs=("p", "q", "s")):
         n = np.ascontiguousarray(n, dtype=np.float64)
-        res = {name: np.empty(n.size) for name in outputs}
+        if n.size >= 1 << 16:  # page-locked outputs: direct device-to-host copies
+            res = dict(zip(outputs, self.ctxs[0]._pinned(n.size, len(outputs))))
+        else:
+            res = {name: np.empty(n.size) for name in outputs}
         arr, nk = self._table(kernels)
         ptr = lambda name: res[name].ctypes.data if name in res else None  # noqa: E731
         with self._lock:

@@ -3320,15 +3320,23 @@ int ttagg_group_rhs(ttagg_group* G, const ttagg_kernel* const* kernels, int n_ke
     if (!std::isfinite(n[j])) return fail(TTAGG_ERR_NONFINITE, "concentration state contains non-finite entries");
   const int64_t Na = (g.N + 31) & ~(int64_t)31;
   const size_t nb = (size_t)g.N * sizeof(double);
-  // pinned staging: [n][p][q][s]
-  if (G->pin_bytes < 4 * Na * sizeof(double)) {
+  // page-locked buffers are transferred directly; pageable ones through the
+  // group's staging area [n][p][q][s]
+  double* outs[3] = {p, q, s};
+  bool stage = !is_pinned(n);
+  for (double* o : outs) stage |= (o && !is_pinned(o));
+  if (stage && G->pin_bytes < 4 * Na * sizeof(double)) {
     if (G->pin) cudaFreeHost(G->pin);
     G->pin = nullptr;
     G->pin_bytes = 0;
     CUDA_TRY(cudaHostAlloc((void**)&G->pin, 4 * Na * sizeof(double), cudaHostAllocDefault));
     G->pin_bytes = 4 * Na * sizeof(double);
   }
-  par_copy(G->pin, n, nb);
+  const double* nsrc = n;
+  if (!is_pinned(n)) {
+    par_copy(G->pin, n, nb);
+    nsrc = G->pin;
+  }
   std::vector<double*> part(G->n);
   for (int i = 0; i < G->n; ++i) {
     ttagg_ctx* c = G->ctx[i];
@@ -3347,20 +3355,22 @@ int ttagg_group_rhs(ttagg_group* G, const ttagg_kernel* const* kernels, int n_ke
       CUDA_TRY(cudaMemsetAsync(part[i], 0, 3 * Na * sizeof(double), G->st[i]));
       continue;
     }
-    CUDA_TRY(cudaMemcpyAsync(nd, G->pin, nb, cudaMemcpyHostToDevice, G->st[i]));
+    CUDA_TRY(cudaMemcpyAsync(nd, nsrc, nb, cudaMemcpyHostToDevice, G->st[i]));
     TRY(ttagg_rhs(c, ks[i].data(), (int)ks[i].size(), nd, part[i], part[i] + Na, part[i] + 2 * Na,
                   TTAGG_WANT_P | TTAGG_WANT_Q, G->st[i]));
   }
   TRY(group_allreduce(G, part, 3 * (size_t)Na));
   CUDA_TRY(cudaSetDevice(G->ctx[0]->device));
-  CUDA_TRY(cudaMemcpyAsync(G->pin + Na, part[0], 3 * Na * sizeof(double), cudaMemcpyDeviceToHost, G->st[0]));
+  for (int j = 0; j < 3; ++j)
+    if (outs[j])
+      CUDA_TRY(cudaMemcpyAsync(is_pinned(outs[j]) ? outs[j] : G->pin + (size_t)(j + 1) * Na, part[0] + (size_t)j * Na,
+                               nb, cudaMemcpyDeviceToHost, G->st[0]));
   for (int i = 0; i < G->n; ++i) {
     CUDA_TRY(cudaSetDevice(G->ctx[i]->device));
     CUDA_TRY(cudaStreamSynchronize(G->st[i]));
   }
-  double* outs[3] = {p, q, s};
   for (int j = 0; j < 3; ++j)
-    if (outs[j]) par_copy(outs[j], G->pin + (size_t)(j + 1) * Na, nb);
+    if (outs[j] && !is_pinned(outs[j])) par_copy(outs[j], G->pin + (size_t)(j + 1) * Na, nb);
   return TTAGG_OK;
 }
 
