@@ -154,8 +154,9 @@ struct ttagg_ctx {
     double2* scratch = nullptr;
     size_t scratch_bytes = 0;
   } work[MAXORD];
-  cudaStream_t s_main = nullptr, s_fill = nullptr;  // mid / least priority
-  cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_fill = nullptr;
+  static constexpr int NFILL = 3;  // cheaper orders' pass B/C, one stream each (least priority)
+  cudaStream_t s_main = nullptr, s_fill[NFILL] = {nullptr, nullptr, nullptr};  // mid / least priority
+  cudaEvent_t ev_fork = nullptr, ev_a = nullptr, ev_fill[NFILL] = {nullptr, nullptr, nullptr};
   int num_sms = 0;
   double* pbuf = nullptr;
   size_t pbuf_bytes = 0;
@@ -2018,9 +2019,11 @@ int make_streams(ttagg_ctx* ctx) {
   int lo = 0, hi = 0;
   CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CUDA_TRY(cudaStreamCreateWithPriority(&ctx->s_main, cudaStreamNonBlocking, (lo + hi) / 2));
-  CUDA_TRY(cudaStreamCreateWithPriority(&ctx->s_fill, cudaStreamNonBlocking, lo));
-  for (cudaEvent_t* e : {&ctx->ev_fork, &ctx->ev_a, &ctx->ev_fill})
-    CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (int i = 0; i < ttagg_ctx::NFILL; ++i) {
+    CUDA_TRY(cudaStreamCreateWithPriority(&ctx->s_fill[i], cudaStreamNonBlocking, lo));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fill[i], cudaEventDisableTiming));
+  }
+  for (cudaEvent_t* e : {&ctx->ev_fork, &ctx->ev_a}) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   return TTAGG_OK;
 }
 
@@ -2128,7 +2131,16 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
     const int big = order[0];
     CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(ctx->s_main, ctx->ev_fork, 0));
-    CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill, ctx->ev_fork, 0));
+    // the cheaper orders are independent: each gets its own fill stream (up to
+    // NFILL; TTAGG_FILL_STREAMS=1 serialises them), so all of them can take
+    // the SMs the costliest order's last pass-B wave leaves idle
+    static int nfill_env = -1;
+    if (nfill_env < 0) {
+      const char* e = getenv("TTAGG_FILL_STREAMS");
+      nfill_env = std::max(1, std::min(ttagg_ctx::NFILL, e ? atoi(e) : ttagg_ctx::NFILL));
+    }
+    const int nfs = std::min(nf - 1, nfill_env);
+    for (int i = 0; i < nfs; ++i) CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill[i], ctx->ev_fork, 0));
     for (int n = nf - 1; n >= 1; --n)  // cheapest first: their pass B/C can start early
       TRY(run_passA(ctx, ks[order[n]], nv, kv, alpha, true, wantQ, ctx->work[order[n]], ctx->s_main));
     // The cheaper orders' pass B/C wait for the costliest order's pass A
@@ -2144,12 +2156,15 @@ int run_orders(ttagg_ctx* ctx, const ttagg_kernel* const* ks, int nk, const doub
     TRY(run_passA(ctx, ks[big], nv, kv, alpha, true, wantQ, ctx->work[big], ctx->s_main));
     if (fill_after) CUDA_TRY(cudaEventRecord(ctx->ev_a, ctx->s_main));
     TRY(run_passBC(ctx, ks[big], pslot(big), ctx->work[big], ctx->s_main));
-    CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill, ctx->ev_a, 0));
-    for (int n = 1; n < nf; ++n) TRY(run_passBC(ctx, ks[order[n]], pslot(order[n]), ctx->work[order[n]], ctx->s_fill));
+    for (int i = 0; i < nfs; ++i) CUDA_TRY(cudaStreamWaitEvent(ctx->s_fill[i], ctx->ev_a, 0));
+    for (int n = 1; n < nf; ++n)
+      TRY(run_passBC(ctx, ks[order[n]], pslot(order[n]), ctx->work[order[n]], ctx->s_fill[(n - 1) % nfs]));
     CUDA_TRY(cudaEventRecord(ctx->ev_a, ctx->s_main));
-    CUDA_TRY(cudaEventRecord(ctx->ev_fill, ctx->s_fill));
     CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_a, 0));
-    CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fill, 0));
+    for (int i = 0; i < nfs; ++i) {
+      CUDA_TRY(cudaEventRecord(ctx->ev_fill[i], ctx->s_fill[i]));
+      CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fill[i], 0));
+    }
   }
   for (int i = 0; i < nk; ++i) {
     const ttagg_kernel* k = ks[i];
@@ -2245,10 +2260,12 @@ int ttagg_ctx_destroy(ttagg_ctx* ctx) {
     cudaFree(w.U);
     cudaFree(w.scratch);
   }
-  for (cudaStream_t x : {ctx->s_main, ctx->s_fill})
-    if (x) cudaStreamDestroy(x);
-  for (cudaEvent_t e : {ctx->ev_a, ctx->ev_fill})
-    if (e) cudaEventDestroy(e);
+  if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
+  if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+  for (int i = 0; i < ttagg_ctx::NFILL; ++i) {
+    if (ctx->s_fill[i]) cudaStreamDestroy(ctx->s_fill[i]);
+    if (ctx->ev_fill[i]) cudaEventDestroy(ctx->ev_fill[i]);
+  }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_last) cudaEventDestroy(ctx->ev_last);
   cudaFree(ctx->pbuf);
