@@ -395,6 +395,16 @@ class Context:
 _CONTEXTS: dict[int, Context] = {}
 
 
+def group_rank_split(d: int, R: int, n_dev: int):
+    """CP rank terms of one order over a device group: LPT (parallel.py's
+    lpt_rank_shards) rotated by the order, so that orders with fewer rank
+    terms than devices land on different devices.  Every rank exactly once."""
+    from .parallel import lpt_rank_shards
+
+    shards = lpt_rank_shards({d: R}, n_dev)
+    return [list(shards[(i + d) % n_dev].get(d, [])) for i in range(n_dev)]
+
+
 class Group:
     """Several GPUs of this process as one rank-sharded engine (ttagg_group_*).
 
@@ -443,13 +453,9 @@ class Group:
             n = len(self.ctxs)
             out = [None] * n
             if hasattr(kernel, "factors"):
-                from .parallel import lpt_rank_shards
-
                 d = len(kernel.factors)
                 R = kernel.factors[0].shape[1]
-                shards = lpt_rank_shards({d: R}, n)
-                for i in range(n):
-                    sub = shards[(i + d) % n].get(d, [])  # rotate so small orders spread out
+                for i, sub in enumerate(group_rank_split(d, R, n)):
                     if sub:
                         out[i] = self.ctxs[i].upload_cp(kernel.factors, rank_subset=sub, dedup=key[1])
             elif hasattr(kernel, "cores"):

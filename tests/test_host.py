@@ -317,3 +317,24 @@ def test_install_routes_reference_cli_through_package_integrate(tmp_path, golden
     finally:
         undo()
     assert tc.integrate is not ti.rhs_total and ti.integrate.__module__ == "ttagg.integrator"
+
+
+def test_group_rank_split_covers_every_rank_once():
+    """Device-group sharding (Group.shards): every CP rank term on exactly one
+    device, balanced within one term, small orders spread over devices."""
+    from paper_1905_09071_b200._lib import group_rank_split
+
+    for n_dev in (1, 2, 3, 4, 8):
+        owners = {}
+        for d, R in ((2, 2), (3, 6), (4, 24), (5, 120)):
+            split = group_rank_split(d, R, n_dev)
+            assert len(split) == n_dev
+            flat = sorted(r for sub in split for r in sub)
+            assert flat == list(range(R))
+            sizes = [len(sub) for sub in split]
+            assert max(sizes) - min(sizes) <= 1
+            for i, sub in enumerate(split):
+                if sub:
+                    owners.setdefault(i, []).append(d)
+        if n_dev == 8:  # the rank-2 and rank-6 orders do not pile onto the same devices
+            assert len(owners) == 8
