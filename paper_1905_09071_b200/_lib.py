@@ -433,13 +433,16 @@ class Group:
         self._lock = threading.RLock()
 
     def close(self):
+        """Free the shards (before their contexts go) and the group."""
         if self.handle:
-            self._cache.clear()
+            with self._lock:
+                for _, shards in self._cache.values():
+                    for dk in shards:
+                        if dk is not None:
+                            dk._fin()  # ttagg_kernel_free now, not at garbage collection
+                self._cache.clear()
             for c in self.ctxs:
                 c._cache.clear()
-            import gc
-
-            gc.collect()
             load().ttagg_group_destroy(self.handle)
             self.handle = None
 
