@@ -389,6 +389,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the D=3 TT (config C4 shape) RHS timing")
     ap.add_argument("--no-extras", action="store_true", help="skip the other configs' timings")
     ap.add_argument("--rk2-steps", type=int, default=50)  # config C5: dt = 0.002, 50 steps
+    ap.add_argument("--launcher-selftest", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--sharded", action="store_true",
                     help="use the rank-sharded multi-GPU code path (perm layout + all-reduce) even at 1 GPU")
     args = ap.parse_args()
@@ -405,6 +406,21 @@ def main():
         print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a mismatched n_gpus",
               file=sys.stderr)
         sys.exit(2)
+    if args.launcher_selftest:  # the launch plumbing alone (gloo, no GPU): tests/test_host.py
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank), float(local), float(world)])
+        got = [torch.zeros(3) for _ in range(world)]
+        dist.all_gather(got, t)
+        ms = torch.tensor([1.0 + rank])
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)  # the max-over-ranks timing reduction
+        if rank == 0:
+            print(json.dumps({"launcher_selftest": True, "n_gpus": world,
+                              "ranks": [[int(x) for x in v.tolist()] for v in got], "max_ms": float(ms)}), flush=True)
+        dist.destroy_process_group()
+        return
 
     from paper_1905_09071_b200.workloads import CONFIGS, initial_state, permutation_power_cp
 

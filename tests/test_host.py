@@ -338,3 +338,27 @@ def test_group_rank_split_covers_every_rank_once():
                     owners.setdefault(i, []).append(d)
         if n_dev == 8:  # the rank-2 and rank-6 orders do not pile onto the same devices
             assert len(owners) == 8
+
+
+def test_bench_launches_its_own_ranks():
+    """`bench.py --gpus N` outside torchrun starts N ranks itself (torchrun on
+    127.0.0.1) and reports n_gpus = the world actually used; a mismatched
+    WORLD_SIZE is refused.  The launch plumbing runs here over gloo
+    (--launcher-selftest: no GPU work)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launcher-selftest"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["max_ms"] == 2.0
+    assert sorted(r[0] for r in line["ranks"]) == [0, 1] and all(r[2] == 2 for r in line["ranks"])
+    bad = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launcher-selftest"],
+                         capture_output=True, text=True, env={**env, "WORLD_SIZE": "1"}, timeout=120)
+    assert bad.returncode == 2 and "refusing" in bad.stderr
