@@ -996,6 +996,169 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
   }
 }
 
+// Pass B for CP kernels with a full pair of prefetch window (N2 = 256, TMA).
+// passB_kernel lands each pair's planes in the row FFTs' exchange buffers, so
+// the next pair can only be requested once both transforms are done (about a
+// quarter of a pair's compute ahead of its use).  Here the staging regions
+// (P and M of one pair, 2 x 32 KB) are separate from the exchange buffer
+// (one 8-row buffer, the two row FFTs run one after the other), and the rank
+// sum lives in tensor memory (64 TMEM columns per CTA: thread = lane, its 16
+// complex sums in its own columns) instead of shared memory, so two CTAs
+// still fit per SM: as soon as every thread holds pair p in registers, pair
+// p+1 is requested and streams in during the whole of pair p's transforms
+// and products.  Same arithmetic in the same order as passB_kernel<256,
+// false, true> (bitwise equal results).
+constexpr int PIPE_STG = 8 * 256;                       // one plane of one row block (double2)
+constexpr int PIPE_EX = 8 * fft_smem_elems(256);        // row FFT exchange (double2)
+constexpr size_t PIPE_SMEM = (size_t)(2 * PIPE_STG + PIPE_EX) * sizeof(double2);
+
+__global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, const __grid_constant__ CUtensorMap tmT) {
+  constexpr int N2 = 256, E = 16, T = 16, SE = fft_smem_elems(N2), ROWS = 8;
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tm_base;
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&tm_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int tid = threadIdx.x;
+  const int rloc = tid & 7, t = tid >> 3;
+  double2* stP = smem;
+  double2* stM = smem + PIPE_STG;
+  double2* ex = smem + 2 * PIPE_STG + rloc * SE;
+  const uint32_t tsum = tm_base + ((uint32_t)(32 * (tid >> 5)) << 16);
+  const int d = a.d, C = a.C;
+  unsigned parity = 0;
+  auto fetch = [&](int rb, int p) {  // one thread: both planes of pair p of row block rb
+    if (tid == 0) {
+      const int xp = a.pmap ? __ldg(a.pmap + p) : p;
+      fence_proxy_async();
+      mbar_expect_tx(&mbar, 2u * ROWS * N2 * sizeof(double2));
+#pragma unroll
+      for (int pl = 0; pl < 2; ++pl)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+            "[%5];" ::"r"(smem_u32(pl ? stM : stP)),
+            "l"(&tmT), "r"(2 * rb * ROWS), "r"(0), "r"(2 * xp + pl), "r"(smem_u32(&mbar))
+            : "memory");
+    }
+  };
+  if (blockIdx.x < a.nrb && a.p0 < a.p1) fetch(blockIdx.x, a.p0);
+  for (int rb = blockIdx.x; rb < a.nrb; rb += gridDim.x) {
+    const int rho = rb * ROWS + rloc;
+    const bool valid = rho < a.K_rows;
+    cplx acc[E];
+    bool have_sum = false;  // the first finished rank term stores, later ones add
+    for (int p = a.p0; p < a.p1; ++p) {
+      cplx vp[E], vm[E];
+      mbar_wait(&mbar, parity);
+      parity ^= 1;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        vp[i] = lds_c(stP + i * 128 + tid);
+        vm[i] = lds_c(stM + i * 128 + tid);
+      }
+      __syncthreads();  // every thread holds pair p: the staging regions are free
+      {
+        const int nrb = rb + (int)gridDim.x;
+        if (p + 1 < a.p1) fetch(rb, p + 1);
+        else if (nrb < a.nrb) fetch(nrb, a.p0);
+      }
+      fft_fwd<N2>(vp, t, ex, a.tw);
+      fft_fwd<N2>(vm, t, ex, a.tw);
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const cplx P = vp[i];
+        vp[i] = cadd(P, vm[i]);
+        vm[i] = mul_mi(csub(P, vm[i]));
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 2 * p + h;
+        if (c >= C) break;
+        const cplx(&X)[E] = h ? vm : vp;
+        const int m = c % d;  // rank-major columns: c = r d + m
+        if (m == 0) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) acc[i] = X[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < E; ++i) acc[i] = cmul(acc[i], X[i]);
+        }
+        if (m == d - 1) {
+          // rank sum += acc, four complex values (16 TMEM columns) at a time
+#pragma unroll
+          for (int q = 0; q < E / 4; ++q) {
+            uint32_t r[16];
+            if (have_sum) {
+              tmem_ld16(tsum + 16 * q, r);
+              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = 4 * q + u;
+              // running sum from exact zero like passB_kernel's Sb (sign of zero included)
+              const cplx old = have_sum ? mk(__hiloint2double((int)r[4 * u + 1], (int)r[4 * u]),
+                                             __hiloint2double((int)r[4 * u + 3], (int)r[4 * u + 2]))
+                                        : mk(0.0, 0.0);
+              const cplx v = cadd(old, acc[i]);
+              r[4 * u + 0] = (uint32_t)__double2loint(v.x);
+              r[4 * u + 1] = (uint32_t)__double2hiint(v.x);
+              r[4 * u + 2] = (uint32_t)__double2loint(v.y);
+              r[4 * u + 3] = (uint32_t)__double2hiint(v.y);
+            }
+            tmem_st16(tsum + 16 * q, r);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          have_sum = true;
+        }
+      }
+    }
+    cplx S[E];
+#pragma unroll
+    for (int q = 0; q < E / 4; ++q) {
+      uint32_t r[16];
+      tmem_ld16(tsum + 16 * q, r);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        S[4 * q + u] = have_sum ? mk(__hiloint2double((int)r[4 * u + 1], (int)r[4 * u]),
+                                     __hiloint2double((int)r[4 * u + 3], (int)r[4 * u + 2]))
+                                : mk(0.0, 0.0);
+    }
+    // (d-1)-position shift, inverse row FFT, inverse twiddle, Hermitian weight (as passB_kernel)
+    const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const long long k = (long long)kap + (long long)a.K * (t + T * i);
+      const long long m = ((long long)(d - 1) * k) % a.L;
+      S[i] = cmul(S[i], twL(a.tabLlo, a.tabLhi, m));
+    }
+    fft_inv<N2>(S, t, ex, a.tw);
+    const double wgt = (kap == 0 || 2 * kap == a.K) ? 1.0 : 2.0;
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int n2 = t + T * i;
+        const cplx u = cscale(cmulc(S[i], twL(a.tabLlo, a.tabLhi, (long long)n2 * kap)), wgt);
+        sts_c(a.U + (size_t)n2 * a.K_rows + rho, u);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tm_base) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // pass C: inverse column transforms, pruned to the sizes 1..N
 // ---------------------------------------------------------------------------
@@ -1672,10 +1835,26 @@ size_t smemB() {
   return (2 * STG + (size_t)ROWS * N2) * sizeof(double2);
 }
 
+// 1: CP pass B with a full pair of prefetch window (passB_pipe_kernel, default);
+// 0: passB_kernel (TTAGG_PASSB_PIPE=0, kept for A/B measurements)
+int passB_pipe() {
+  static const int mode = [] {
+    const char* e = getenv("TTAGG_PASSB_PIPE");
+    return e ? atoi(e) : 1;
+  }();
+  return mode;
+}
+
 template <int N2, bool TT>
 int launchB(const PassBArgs& a, const CUtensorMap* tm, int grid, cudaStream_t st) {
   const size_t smem = smemB<N2>();
   if constexpr (N2 == 256) {
+    if (tm && !TT && passB_pipe()) {
+      TRY(set_smem(passB_pipe_kernel, PIPE_SMEM));
+      passB_pipe_kernel<<<grid, 128, PIPE_SMEM, st>>>(a, *tm);
+      CUDA_TRY(cudaGetLastError());
+      return TTAGG_OK;
+    }
     if (tm) {
       TRY(set_smem(passB_kernel<N2, TT, true>, smem));
       passB_kernel<N2, TT, true><<<grid, 128, smem, st>>>(a, *tm);

@@ -22,3 +22,22 @@ print("ctx._pinned(N, 3)           %.2f ms" % tm(lambda: ctx._pinned(N, 3)))
 print("ctx.rhs_host(dks, n)        %.2f ms" % tm(lambda: ctx.rhs_host(dks, n0)))
 print("g.rhs_total(ks, st)         %.2f ms" % tm(lambda: g.rhs_total(ks, st)))
 print("state+rhs_total             %.2f ms" % tm(lambda: g.rhs_total(ks, g.ConcentrationState(n0))))
+# the library alone: pinned state in, pinned outputs reused (no Python allocation)
+import ctypes, torch
+from paper_1905_09071_b200._lib import load, _vp, TTAGG_HOST_PTRS, TTAGG_WANT_P, TTAGG_WANT_Q
+lib = load()
+nin = torch.from_numpy(n0.copy()).pin_memory().numpy()
+outs = [torch.empty(N, dtype=torch.float64, pin_memory=True).numpy() for _ in range(3)]
+arr = (_vp * len(dks))(*[k.handle for k in dks])
+fl = TTAGG_HOST_PTRS | TTAGG_WANT_P | TTAGG_WANT_Q
+raw = lambda: lib.ttagg_rhs(ctx.handle, arr, len(dks), nin.ctypes.data, outs[0].ctypes.data, outs[1].ctypes.data, outs[2].ctypes.data, fl, None)
+print("raw ttagg_rhs pinned in/out %.2f ms" % tm(raw))
+dev = torch.device("cuda", 0)
+nd = torch.from_numpy(n0).to(dev); pd = torch.empty(3 * N, dtype=torch.float64, device=dev)
+def devonly():
+    ctx.rhs_device(dks, nd.data_ptr(), pd.data_ptr(), pd.data_ptr() + 8 * N, pd.data_ptr() + 16 * N,
+                   torch.cuda.current_stream(dev).cuda_stream)
+    torch.cuda.synchronize(dev)
+print("device ptrs + sync          %.2f ms" % tm(devonly))
+print("raw ttagg_rhs pinned in/out %.2f ms (again)" % tm(raw))
+print("g.rhs_total(ks, st)         %.2f ms (again)" % tm(lambda: g.rhs_total(ks, st)))
