@@ -212,10 +212,69 @@ __device__ __forceinline__ void twiddle16(cplx* x, cplx w1, cplx w4) {
   x[15] = cmul(x[15], cmul(w12, w3));
 }
 
+// ---- tensor memory (TMEM) as per-thread storage (tcgen05.alloc / st / ld,
+// 32x32b shape: a thread reads and writes the columns of its own lane; warp w
+// of a CTA owns lanes 32 (w % 4) .. +31)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Stage twiddles kept in tensor memory: the 15 powers w^1..w^15 of a
+// twiddled radix-16 stage depend on the thread only (w = W_{16 NS}^(t mod NS)),
+// so a persistent CTA stores them once (64 TMEM columns per stage: slot i =
+// w^i, slot 0 unused) and every transform reads them back instead of
+// rebuilding them from w^1 and w^4 (13 complex products per stage).
+constexpr uint32_t TMW_NONE = 0xffffffffu;
+__device__ __forceinline__ void tmem_store_twiddles16(uint32_t taddr, const double2* __restrict__ tw, int e) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t r[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 w = tw[((4 * q + u) * e) & (4096 - 1)];
+      r[4 * u + 0] = (uint32_t)__double2loint(w.x);
+      r[4 * u + 1] = (uint32_t)__double2hiint(w.x);
+      r[4 * u + 2] = (uint32_t)__double2loint(w.y);
+      r[4 * u + 3] = (uint32_t)__double2hiint(w.y);
+    }
+    tmem_st16(taddr + 16 * q, r);
+  }
+  tmem_wait_st();
+}
+__device__ __forceinline__ void twiddle16_tmem(cplx* x, uint32_t taddr) {
+  uint32_t r[4][16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) tmem_ld16(taddr + 16 * q, r[q]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    const int q = i >> 2, u = i & 3;
+    const cplx w = mk(__hiloint2double((int)r[q][4 * u + 1], (int)r[q][4 * u]),
+                      __hiloint2double((int)r[q][4 * u + 3], (int)r[q][4 * u + 2]));
+    x[i] = cmul(x[i], w);
+  }
+}
+
 // One stage.  Registers: element t + T*r in v[r] on entry (read pattern).
 template <int M, int R, int NS, bool LAST>
 __device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
-                                          const double2* stw = nullptr) {
+                                          const double2* stw = nullptr, uint32_t tmw = TMW_NONE) {
   constexpr int E = fft_e(M);
   constexpr int T = fft_t(M);
   constexpr int G = E / R;  // butterflies per thread
@@ -233,7 +292,8 @@ __device__ __forceinline__ void fft_stage(cplx (&v)[fft_e(M)], int t, double2* s
 #define TTAGG_TW_MODE 0
 #endif
       if constexpr (R == 16 && TTAGG_TW_MODE == 0) {
-        if (stw) twiddle16(x, lds_c(stw + qm), lds_c(stw + NS + qm));
+        if (tmw != TMW_NONE) twiddle16_tmem(x, tmw);
+        else if (stw) twiddle16(x, lds_c(stw + qm), lds_c(stw + NS + qm));
         else twiddle16(x, ld_c(tw + e), ld_c(tw + 4 * e));
       } else if constexpr (R == 16 && TTAGG_TW_MODE == 2) {
         // w1..w3 and w4, w8, w12 loaded; 9 products
@@ -367,7 +427,8 @@ __device__ __forceinline__ void fft_fwd2(cplx (&v1)[fft_e(M)], cplx (&v2)[fft_e(
 // ---------------------------------------------------------------------------
 template <int M, int R, int NS, class Sync>
 __device__ __forceinline__ void fft_stage_split(cplx (&v)[fft_e(M)], int t, double* sm, const double2* __restrict__ tw,
-                                                const Sync& sync, const double2* stw = nullptr) {
+                                                const Sync& sync, const double2* stw = nullptr,
+                                                uint32_t tmw = TMW_NONE) {
   constexpr int E = fft_e(M);
   constexpr int T = fft_t(M);
   constexpr int G = E / R;
@@ -382,7 +443,8 @@ __device__ __forceinline__ void fft_stage_split(cplx (&v)[fft_e(M)], int t, doub
       const int qm = q & (NS - 1);
       const int e = qm * (TW_BASE / (NS * R));
       if constexpr (R == 16) {
-        if (stw) twiddle16(x, lds_c(stw + qm), lds_c(stw + NS + qm));
+        if (tmw != TMW_NONE) twiddle16_tmem(x, tmw);
+        else if (stw) twiddle16(x, lds_c(stw + qm), lds_c(stw + NS + qm));
         else twiddle16(x, ld_c(tw + e), ld_c(tw + 4 * e));
       } else {
 #pragma unroll
@@ -438,7 +500,8 @@ __device__ __forceinline__ void fft_stage_table(double2* stw, const double2* __r
 
 template <int M, class Sync = CtaSync>
 __device__ __forceinline__ void fft_fwd_split(cplx (&v)[fft_e(M)], int t, double* sm, const double2* __restrict__ tw,
-                                              const Sync& sync = Sync(), const double2* stw = nullptr) {
+                                              const Sync& sync = Sync(), const double2* stw = nullptr,
+                                              uint32_t tmw = TMW_NONE) {
   static_assert(M >= 256 && M <= 4096, "block transforms");
   constexpr int b = fft_first_radix(M);
   constexpr int a = (ilog2c(M) - ilog2c(b)) / 4;
@@ -446,13 +509,18 @@ __device__ __forceinline__ void fft_fwd_split(cplx (&v)[fft_e(M)], int t, double
   if constexpr (b > 1) fft_stage_split<M, b, 1>(v, t, sm, tw, sync);
   constexpr int NS1 = b;
   if constexpr (a == 2) {
-    fft_stage_split<M, 16, NS1>(v, t, sm, tw, sync, stw);
-    fft_stage<M, 16, NS1 * 16, true>(v, t, nullptr, tw, stw ? stw + off : nullptr);
+    // tmw (M >= 256 with b == 1 only): stage NS = 16 at tmw, nothing else twiddled
+    fft_stage_split<M, 16, NS1>(v, t, sm, tw, sync, stw, b == 1 ? TMW_NONE : tmw);
+    fft_stage<M, 16, NS1 * 16, true>(v, t, nullptr, tw, stw ? stw + off : nullptr,
+                                     tmw == TMW_NONE ? TMW_NONE : tmw + (b == 1 ? 0 : 64));
   } else {
     static_assert(a == 3, "M <= 4096");
+    // tmw: the two twiddled stages (NS = 16 b, 256 b) read their per-thread
+    // twiddles from tensor memory columns tmw + 0 and tmw + 64
     fft_stage_split<M, 16, NS1>(v, t, sm, tw, sync);
-    fft_stage_split<M, 16, NS1 * 16>(v, t, sm, tw, sync, stw);
-    fft_stage<M, 16, NS1 * 256, true>(v, t, nullptr, tw, stw ? stw + off : nullptr);
+    fft_stage_split<M, 16, NS1 * 16>(v, t, sm, tw, sync, stw, tmw);
+    fft_stage<M, 16, NS1 * 256, true>(v, t, nullptr, tw, stw ? stw + off : nullptr,
+                                      tmw == TMW_NONE ? TMW_NONE : tmw + 64);
   }
 }
 

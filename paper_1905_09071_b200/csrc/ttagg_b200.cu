@@ -274,6 +274,9 @@ struct PMOut {
   cplx cn2;     // W_L^(n2 K) = W_N2^(n2)
 };
 
+#ifndef TTAGG_A_TMEMTW
+#define TTAGG_A_TMEMTW 1
+#endif
 #ifndef TTAGG_B_JOINT
 #define TTAGG_B_JOINT 1
 #endif
@@ -517,8 +520,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
 // instead of re-reading the columns through L1/L2.  To fit z (N1 x 16 B) and
 // the transform's exchange in two CTAs per SM, exchanges go through a
 // half-size buffer in two rounds (fft_fwd_split).
+// stage twiddles in tensor memory: CTAs of 4 or 8 warps (N1 = 2048, 4096); the
+// column budget (512 per SM) holds for their 4 resp. 2 resident CTAs
+__host__ __device__ constexpr bool passA_tmem_twiddles(int N1) { return TTAGG_A_TMEMTW && fft_t(N1) >= 128; }
+__host__ __device__ constexpr unsigned passA_tmem_cols(int N1) { return fft_t(N1) >= 256 ? 256u : 128u; }
+
+// resident CTAs per SM the register budget is sized for: 16 warps per SM
+#ifndef TTAGG_A_WARPS
+#define TTAGG_A_WARPS 16
+#endif
+__host__ __device__ constexpr int passA_min_ctas(int N1) {
+  return fft_t(N1) >= 256 ? 2 : (TTAGG_A_WARPS * 32) / fft_t(N1);
+}
+
 template <int N1>
-__global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs a, int nitems) {
+__global__ void __launch_bounds__(fft_t(N1), passA_min_ctas(N1)) passA_tma_kernel(const PassAArgs a, int nitems) {
   constexpr int E = fft_e(N1), T = fft_t(N1);
   constexpr int NW = T / 32;
   constexpr unsigned ROW_BYTES = N1 * sizeof(double2);
@@ -534,6 +550,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
   __shared__ double2 Kst[MAXRES][16];
   __shared__ int rbase[MAXRES];
   __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tm_base;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int d = a.d;
   const int N2 = a.N2;
@@ -546,7 +563,31 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
     Kst[j][r] = make_double2(w.x, w.y);
   }
   if (t < MAXRES) rbase[t] = a.res_base[t];
-  fft_stage_table<N1>(stw, a.tw, t, T);
+  // Stage twiddles: the 15 powers a thread needs in each of the two twiddled
+  // radix-16 stages never change, so CTAs of >= 4 warps park them in tensor
+  // memory once (128 columns per thread: 64 per stage; warps w and w + 4
+  // share a lane quadrant and take different column halves) and every
+  // transform reads them back (tcgen05.ld) instead of rebuilding them from
+  // two table values; smaller CTAs keep the shared stage table.
+  uint32_t tmw = TMW_NONE;
+  if constexpr (passA_tmem_twiddles(N1)) {
+    constexpr unsigned TCOLS = passA_tmem_cols(N1);
+    if (wid == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tm_base)),
+                   "n"(TCOLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tmw = tm_base + ((uint32_t)(32 * (wid & 3)) << 16) + 128u * (uint32_t)(wid >> 2);
+    constexpr int NSa = fft_stage_ns<N1>(0), NSb = fft_stage_ns<N1>(1);
+    tmem_store_twiddles16(tmw, a.tw, (t & (NSa - 1)) * (TW_BASE / (NSa * 16)));
+    tmem_store_twiddles16(tmw + 64, a.tw, (t & (NSb - 1)) * (TW_BASE / (NSb * 16)));
+  } else {
+    fft_stage_table<N1>(stw, a.tw, t, T);
+  }
   auto issue = [&](int it) {  // one thread: bulk-copy item it's row into zs
     const int pair = a.pair0 + it / N2, n2 = it % N2;
     const double2* src = X2 + (size_t)pair * Np + (size_t)n2 * N1;
@@ -633,7 +674,7 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
       continue;
     }
     // residue 0 straight from the registers
-    fft_fwd_split<N1>(z, t, ex, a.tw, CtaSync(), stw);
+    fft_fwd_split<N1>(z, t, ex, a.tw, CtaSync(), stw, tmw);
     emit_split<N1>(rbase, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
     for (int j = 1; j < d; ++j) {
       cplx v[E];
@@ -644,32 +685,20 @@ __global__ void __launch_bounds__(fft_t(N1), 2) passA_tma_kernel(const PassAArgs
         __syncthreads();  // zs free: the next item's row can land while this residue transforms
         if (t == 0 && next < nitems) issue(next);
       }
-      fft_fwd_split<N1>(v, t, ex, a.tw, CtaSync(), stw);
+      fft_fwd_split<N1>(v, t, ex, a.tw, CtaSync(), stw, tmw);
       emit_split<N1>(rbase, o, d, j, t, v, cmul(ct, lds_c(&Ust[pb][j])), Pst[pb], PMst[pb]);
     }
   }
+  if constexpr (passA_tmem_twiddles(N1)) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (wid == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base), "n"(passA_tmem_cols(N1))
+                   : "memory");
+  }
 }
 
-// ---- tensor memory (TMEM) as per-thread storage (tcgen05.alloc / st / ld):
-// 16 complex values <-> 64 TMEM columns of the thread's lane (32x32b shape:
-// warp w of a 4-warp CTA owns lanes 32w..32w+31)
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-}
+// (tensor-memory helpers tmem_st16 / tmem_ld16 live in fft.cuh)
 // ---------------------------------------------------------------------------
 // pass B: row FFTs, spectral product / chain, inverse row FFTs
 // ---------------------------------------------------------------------------
@@ -1772,7 +1801,7 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
     for (int j = 0; j < a.d; ++j) halves = halves && a.res_cnt[j] == N1 / 2 + (j == 0);
     if (passA_mode() == 1 && halves) {
       const size_t smem = (size_t)N1 * sizeof(double2) + (size_t)((fft_smem_elems(N1) + 1) & ~1) * sizeof(double) +
-                          (size_t)fft_stage_table_elems<N1>() * sizeof(double2);
+                          (passA_tmem_twiddles(N1) ? 0 : (size_t)fft_stage_table_elems<N1>() * sizeof(double2));
       TRY(set_smem(passA_tma_kernel<N1>, smem));
       static int resident[64] = {0};  // CTAs per SM x SMs, per device
       int dev = 0;
@@ -1782,6 +1811,18 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
         int sms = 0, occ = 0;
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passA_tma_kernel<N1>, T, smem));
+        if (passA_tmem_twiddles(N1)) {
+          // the occupancy query answers 1 for a kernel that allocates tensor
+          // memory; the CTAs the launch bounds and the shared memory allow do
+          // become resident (their column requests sum to <= 512)
+          cudaFuncAttributes fa;
+          int smem_sm = 0;
+          CUDA_TRY(cudaFuncGetAttributes(&fa, passA_tma_kernel<N1>));
+          CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+          const int by_smem = (int)((size_t)smem_sm / (smem + fa.sharedSizeBytes + 1024));
+          const int by_tmem = 512 / (int)passA_tmem_cols(N1);
+          occ = std::max(occ, std::min(passA_min_ctas(N1), std::min(by_smem, by_tmem)));
+        }
         resident[dev] = std::max(1, occ) * sms;
       }
       const int nitems = npairs * N2;

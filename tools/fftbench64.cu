@@ -118,9 +118,27 @@ void run_res(double2* out, double2* tw) {
 
 // The same loop on the [16,16,16] block as pass A uses it today: 256 threads,
 // two CTAs per SM, z in shared memory, split exchanges.
+template <bool TM>
 __global__ void __launch_bounds__(256, 2) bench_res_old(double2* out, const double2* tw, int iters) {
   extern __shared__ __align__(16) double2 sm2[];
   const int t = threadIdx.x;
+  __shared__ uint32_t tm_base;
+  uint32_t tmw = TMW_NONE;
+  if constexpr (TM) {
+    if ((t >> 5) == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&tm_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int w = t >> 5;
+    tmw = tm_base + ((uint32_t)(32 * (w & 3)) << 16) + 128u * (w >> 2);
+    tmem_store_twiddles16(tmw, tw, (t & 15) * 16);
+    tmem_store_twiddles16(tmw + 64, tw, t);
+  }
   double2* zs = sm2;
   double* ex = reinterpret_cast<double*>(sm2 + 4096);
   __shared__ double2 Kst[16], Pst[16];
@@ -136,26 +154,32 @@ __global__ void __launch_bounds__(256, 2) bench_res_old(double2* out, const doub
     cplx v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = cmul(lds_c(zs + t + 256 * r), cmul(tb, lds_c(Kst + r)));
-    fft_fwd_split<4096>(v, t, ex, tw, CtaSync());
+    fft_fwd_split<4096>(v, t, ex, tw, CtaSync(), nullptr, tmw);
     double2* oo = o + (it & 1) * 4096;
 #pragma unroll
     for (int r = 0; r < 16; ++r) sts_c(oo + t + 256 * r, cmul(v[r], cmul(tb, lds_c(Pst + r))));
   }
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if ((t >> 5) == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm_base) : "memory");
+  }
 }
+template <bool TM>
 void run_res_old(double2* out, double2* tw, int per_sm) {
   const size_t smem = per_sm == 1 ? 120 * 1024 : 65536 + (fft_smem_elems(4096) + 1) * 8;
-  cudaFuncSetAttribute(bench_res_old, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(bench_res_old<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bench_res_old, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bench_res_old<TM>, 256, smem);
   const int grid = 148 * per_sm, iters = 400;
-  bench_res_old<<<grid, 256, smem>>>(out, tw, 2);
+  bench_res_old<TM><<<grid, 256, smem>>>(out, tw, 2);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   cudaEventRecord(a);
-  bench_res_old<<<grid, 256, smem>>>(out, tw, iters);
+  bench_res_old<TM><<<grid, 256, smem>>>(out, tw, iters);
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
   const double pts = (double)grid * 4096 * iters;
-  printf("res_old 256thr smem=%zu occ=%d/SM: %.3f ms %.2f clk/pt/SM err=%s\n", smem, nb, ms,
+  printf("res_old tmem_tw=%d 256thr smem=%zu occ=%d/SM: %.3f ms %.2f clk/pt/SM err=%s\n", (int)TM, smem, nb, ms,
          148 * 1.965e9 * (ms * 1e-3) / pts, cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -232,8 +256,12 @@ int main() {
   run_wide<2>(out, tw);
   run_wide<3>(out, tw);
   run_wide<4>(out, tw);
-  run_res_old(out, tw, 2);
-  run_res_old(out, tw, 1);
+  run_res_old<false>(out, tw, 2);
+  run_res_old<true>(out, tw, 2);
+  run_res_old<false>(out, tw, 2);
+  run_res_old<true>(out, tw, 2);
+  run_res_old<false>(out, tw, 1);
+  run_res_old<true>(out, tw, 1);
   run_res<2>(out, tw);
   run_res<3>(out, tw);
   run_res<4>(out, tw);
