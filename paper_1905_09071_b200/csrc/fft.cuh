@@ -337,7 +337,8 @@ __host__ __device__ constexpr int fft_stage_ns(int which);
 
 template <int M, class Sync = CtaSync>
 __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
-                                        const Sync& sync = Sync(), const double2* stw = nullptr) {
+                                        const Sync& sync = Sync(), const double2* stw = nullptr,
+                                        uint32_t tmw = TMW_NONE) {
   if constexpr (M <= 16) {
     DFT<M>::run(v);
     // DFT<R> leaves natural order, and with T == 1 register r == frequency r
@@ -361,7 +362,9 @@ __device__ __forceinline__ void fft_fwd(cplx (&v)[fft_e(M)], int t, double2* sm,
       sync();
       fft_load_regs<M>(v, t, sm);
       sync();
-      fft_stage<M, 16, NS1 * 16, true>(v, t, sm, tw, stw ? stw + 2 * fft_stage_ns<M>(0) : nullptr);
+      // tmw (b == 1 only): the one twiddled stage reads its twiddles from tensor memory
+      fft_stage<M, 16, NS1 * 16, true>(v, t, sm, tw, stw ? stw + 2 * fft_stage_ns<M>(0) : nullptr,
+                                       b == 1 ? tmw : TMW_NONE);
     } else {
       static_assert(a == 3, "M <= 4096");
       fft_stage<M, 16, NS1, false>(v, t, sm, tw);
@@ -527,11 +530,11 @@ __device__ __forceinline__ void fft_fwd_split(cplx (&v)[fft_e(M)], int t, double
 // Inverse (unnormalised) via conj(FFT(conj(x))).
 template <int M, class Sync = CtaSync>
 __device__ __forceinline__ void fft_inv(cplx (&v)[fft_e(M)], int t, double2* sm, const double2* __restrict__ tw,
-                                        const Sync& sync = Sync()) {
+                                        const Sync& sync = Sync(), uint32_t tmw = TMW_NONE) {
   constexpr int E = fft_e(M);
 #pragma unroll
   for (int r = 0; r < E; ++r) v[r].y = -v[r].y;
-  fft_fwd<M, Sync>(v, t, sm, tw, sync);
+  fft_fwd<M, Sync>(v, t, sm, tw, sync, nullptr, tmw);
 #pragma unroll
   for (int r = 0; r < E; ++r) v[r].y = -v[r].y;
 }
