@@ -258,6 +258,7 @@ struct PassAArgs {
   const double2* tabLhi;
   int d, N2, K_rows, nblk, want_T;
   int pair0;  // first column pair of this launch (pass-A chunk)
+  int raw;    // exchange rows leave without the four-step twiddle (pass B applies it; raw_exchange())
   int res_base[MAXRES], res_cnt[MAXRES];
 };
 
@@ -320,6 +321,25 @@ __device__ __forceinline__ void emit_split(const int* rbase, const PMOut& o, int
   if (t == 0 && j == 0) {
     sts_c(o.TM + rbase[0], cconj(v[0]));
     sts_c(TP + T * 8, cmul(v[8], cmul(b, lds_c(Pst + 8))));
+  }
+}
+
+// emit_split for a raw exchange (raw_exchange()): the four-step twiddle
+// W_L^(n2 kappa) is the same for the P row kappa and the M row kappa (see
+// emit_pm), depends on (row, n2) only and not on the column pair, so pass B
+// applies it from per-thread constants and pass A stores Y resp. conj(Y).
+template <int N1>
+__device__ __forceinline__ void emit_raw(const int* rbase, const PMOut& o, int d, int j, int t, const cplx (&v)[16]) {
+  constexpr int T = N1 / 16;
+  double2* TP = o.TP + rbase[j];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) sts_c(TP + t + T * r, v[r]);
+  double2* TM = j == 0 ? o.TM + rbase[0] + N1 - t : o.TM + rbase[d - j] + (N1 - 1 - t);
+#pragma unroll
+  for (int r = 8; r < 16; ++r) sts_c(TM - T * r, cconj(v[r]));
+  if (t == 0 && j == 0) {
+    sts_c(o.TM + rbase[0], cconj(v[0]));
+    sts_c(TP + T * 8, v[8]);
   }
 }
 
@@ -533,7 +553,7 @@ __host__ __device__ constexpr int passA_min_ctas(int N1) {
   return fft_t(N1) >= 256 ? 2 : (TTAGG_A_WARPS * 32) / fft_t(N1);
 }
 
-template <int N1>
+template <int N1, bool RAW>
 __global__ void __launch_bounds__(fft_t(N1), passA_min_ctas(N1)) passA_tma_kernel(const PassAArgs a, int nitems) {
   constexpr int E = fft_e(N1), T = fft_t(N1);
   constexpr int NW = T / 32;
@@ -611,23 +631,26 @@ __global__ void __launch_bounds__(fft_t(N1), passA_min_ctas(N1)) passA_tma_kerne
     const double* nv = a.nv + e0;
     const double* kv = a.kv ? a.kv + e0 : nullptr;
     const int pb = it_n & 1;
-    if (t < 16) {
-      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * t);
-      Pst[pb][t] = make_double2(w.x, w.y);
-    } else if (t < 16 + d) {
-      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * (t - 16));
-      Ust[pb][t - 16] = make_double2(w.x, w.y);
-    }
-    // emit twiddle W_L^(n2 (j + d t)) = W_L^(n2 d t) W_L^(n2 j)
-    const cplx ct = twL(a.tabLlo, a.tabLhi, (long long)n2 * (d * t));
     PMOut o;
     o.TP = a.T + (size_t)pair * 2 * plane + (size_t)n2 * a.K_rows;
     o.TM = o.TP + plane;
-    o.cn2 = twL(a.tabLlo, a.tabLhi, (long long)n2 * K);
-    if (t >= 32 && t < 48) {
-      const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * (t - 32));
-      const cplx pm = cmul(cconj(w), o.cn2);
-      PMst[pb][t - 32] = make_double2(pm.x, pm.y);
+    cplx ct = mk(1.0, 0.0);
+    if constexpr (!RAW) {
+      if (t < 16) {
+        const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * t);
+        Pst[pb][t] = make_double2(w.x, w.y);
+      } else if (t < 16 + d) {
+        const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * (t - 16));
+        Ust[pb][t - 16] = make_double2(w.x, w.y);
+      }
+      // emit twiddle W_L^(n2 (j + d t)) = W_L^(n2 d t) W_L^(n2 j)
+      ct = twL(a.tabLlo, a.tabLhi, (long long)n2 * (d * t));
+      o.cn2 = twL(a.tabLlo, a.tabLhi, (long long)n2 * K);
+      if (t >= 32 && t < 48) {
+        const cplx w = twL(a.tabLlo, a.tabLhi, (long long)n2 * d * T * (t - 32));
+        const cplx pm = cmul(cconj(w), o.cn2);
+        PMst[pb][t - 32] = make_double2(pm.x, pm.y);
+      }
     }
     // the state weights of this n2 row (through L1; shared by every pair)
     double wv[E];
@@ -675,7 +698,8 @@ __global__ void __launch_bounds__(fft_t(N1), passA_min_ctas(N1)) passA_tma_kerne
     }
     // residue 0 straight from the registers
     fft_fwd_split<N1>(z, t, ex, a.tw, CtaSync(), stw, tmw);
-    emit_split<N1>(rbase, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
+    if constexpr (RAW) emit_raw<N1>(rbase, o, d, 0, t, z);
+    else emit_split<N1>(rbase, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
     for (int j = 1; j < d; ++j) {
       cplx v[E];
       const cplx tb = ld_c(a.tabK + j * t);
@@ -686,7 +710,8 @@ __global__ void __launch_bounds__(fft_t(N1), passA_min_ctas(N1)) passA_tma_kerne
         if (t == 0 && next < nitems) issue(next);
       }
       fft_fwd_split<N1>(v, t, ex, a.tw, CtaSync(), stw, tmw);
-      emit_split<N1>(rbase, o, d, j, t, v, cmul(ct, lds_c(&Ust[pb][j])), Pst[pb], PMst[pb]);
+      if constexpr (RAW) emit_raw<N1>(rbase, o, d, j, t, v);
+      else emit_split<N1>(rbase, o, d, j, t, v, cmul(ct, lds_c(&Ust[pb][j])), Pst[pb], PMst[pb]);
     }
   }
   if constexpr (passA_tmem_twiddles(N1)) {
@@ -717,6 +742,7 @@ struct PassBArgs {
   int ranks[MAXD + 1];
   const int* fdesc;  // TT: per uploaded fiber, packed (core, rn, rp, first, last, noop)
   const int* pmap;   // deduplicated CP: stored exchange pair of each pair (null: identity)
+  int raw;           // the exchange holds untwiddled column outputs: multiply by W_L^(n2 kappa) here
 };
 
 // TT fiber descriptor: the uploaded columns are the live fibers only (all-zero
@@ -1047,7 +1073,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tm_base;
   if ((threadIdx.x >> 5) == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&tm_base))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tm_base))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -1064,6 +1090,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
   double2* stM = smem + PIPE_STG;
   double2* ex = smem + 2 * PIPE_STG + rloc * SE;
   const uint32_t tsum = tm_base + ((uint32_t)(32 * (tid >> 5)) << 16);
+  const uint32_t tfs = tsum + 64;  // raw exchange: this thread's four-step twiddles W_L^(n2 kappa), n2 = t + 16 i
   const int d = a.d, C = a.C;
   unsigned parity = 0;
   auto fetch = [&](int rb, int p) {  // one thread: both planes of pair p of row block rb
@@ -1084,16 +1111,62 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
   for (int rb = blockIdx.x; rb < a.nrb; rb += gridDim.x) {
     const int rho = rb * ROWS + rloc;
     const bool valid = rho < a.K_rows;
+    const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
+    if (a.raw) {
+      // the row's four-step twiddles are the same for every pair: built once
+      // per row block, parked in tensor memory (16 complex = 64 columns)
+#pragma unroll
+      for (int q = 0; q < E / 4; ++q) {
+        uint32_t r[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const cplx w = twL(a.tabLlo, a.tabLhi, (long long)(t + T * (4 * q + u)) * kap);
+          r[4 * u + 0] = (uint32_t)__double2loint(w.x);
+          r[4 * u + 1] = (uint32_t)__double2hiint(w.x);
+          r[4 * u + 2] = (uint32_t)__double2loint(w.y);
+          r[4 * u + 3] = (uint32_t)__double2hiint(w.y);
+        }
+        tmem_st16(tfs + 16 * q, r);
+      }
+      tmem_wait_st();
+    }
     cplx acc[E];
     bool have_sum = false;  // the first finished rank term stores, later ones add
     for (int p = a.p0; p < a.p1; ++p) {
       cplx vp[E], vm[E];
+      // raw exchange: the row's four-step twiddles come back from tensor memory
+      // (two 4-value chunks in flight) while the pair's planes are still landing,
+      // and multiply the values as they leave the staging regions
+      uint32_t fs[2][16];
+      if (a.raw) {
+        tmem_ld16(tfs, fs[0]);
+        tmem_ld16(tfs + 16, fs[1]);
+      }
       mbar_wait(&mbar, parity);
       parity ^= 1;
+      if (a.raw) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        vp[i] = lds_c(stP + i * 128 + tid);
-        vm[i] = lds_c(stM + i * 128 + tid);
+        for (int q = 0; q < E / 4; ++q) {
+          if (q == 0 || q == 2) tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = 4 * q + u;
+            const cplx w = mk(__hiloint2double((int)fs[q & 1][4 * u + 1], (int)fs[q & 1][4 * u]),
+                              __hiloint2double((int)fs[q & 1][4 * u + 3], (int)fs[q & 1][4 * u + 2]));
+            vp[i] = cmul(lds_c(stP + i * 128 + tid), w);
+            vm[i] = cmul(lds_c(stM + i * 128 + tid), w);
+          }
+          if (q == 1) {
+            tmem_ld16(tfs + 32, fs[0]);
+            tmem_ld16(tfs + 48, fs[1]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          vp[i] = lds_c(stP + i * 128 + tid);
+          vm[i] = lds_c(stM + i * 128 + tid);
+        }
       }
       __syncthreads();  // every thread holds pair p: the staging regions are free
       {
@@ -1164,7 +1237,6 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
                                 : mk(0.0, 0.0);
     }
     // (d-1)-position shift, inverse row FFT, inverse twiddle, Hermitian weight (as passB_kernel)
-    const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const long long k = (long long)kap + (long long)a.K * (t + T * i);
@@ -1185,7 +1257,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if ((threadIdx.x >> 5) == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tm_base) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_base) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1802,7 +1874,8 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
     if (passA_mode() == 1 && halves) {
       const size_t smem = (size_t)N1 * sizeof(double2) + (size_t)((fft_smem_elems(N1) + 1) & ~1) * sizeof(double) +
                           (passA_tmem_twiddles(N1) ? 0 : (size_t)fft_stage_table_elems<N1>() * sizeof(double2));
-      TRY(set_smem(passA_tma_kernel<N1>, smem));
+      auto kern = a.raw ? passA_tma_kernel<N1, true> : passA_tma_kernel<N1, false>;
+      TRY(set_smem(kern, smem));
       static int resident[64] = {0};  // CTAs per SM x SMs, per device
       int dev = 0;
       CUDA_TRY(cudaGetDevice(&dev));
@@ -1810,14 +1883,14 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
       if (!resident[dev]) {
         int sms = 0, occ = 0;
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passA_tma_kernel<N1>, T, smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passA_tma_kernel<N1, false>, T, smem));
         if (passA_tmem_twiddles(N1)) {
           // the occupancy query answers 1 for a kernel that allocates tensor
           // memory; the CTAs the launch bounds and the shared memory allow do
           // become resident (their column requests sum to <= 512)
           cudaFuncAttributes fa;
           int smem_sm = 0;
-          CUDA_TRY(cudaFuncGetAttributes(&fa, passA_tma_kernel<N1>));
+          CUDA_TRY(cudaFuncGetAttributes(&fa, passA_tma_kernel<N1, false>));
           CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
           const int by_smem = (int)((size_t)smem_sm / (smem + fa.sharedSizeBytes + 1024));
           const int by_tmem = 512 / (int)passA_tmem_cols(N1);
@@ -1827,11 +1900,12 @@ int launchA(const PassAArgs& a, int N2, int npairs, cudaStream_t st) {
       }
       const int nitems = npairs * N2;
       const int grid = std::max(1, std::min(nitems, resident[dev]));
-      passA_tma_kernel<N1><<<grid, T, smem, st>>>(a, nitems);
+      kern<<<grid, T, smem, st>>>(a, nitems);
       CUDA_TRY(cudaGetLastError());
       return TTAGG_OK;
     }
   }
+  if (a.raw) return fail(TTAGG_ERR_UNSUPPORTED, "raw exchange needs the TMA-fed pass A");
   if constexpr (T >= 32) {
     const size_t smem = (size_t)fft_smem_elems(N1) * sizeof(double2);
     TRY(set_smem(passA_big_kernel<N1>, smem));
@@ -2029,6 +2103,20 @@ struct ProfScope {
   }
 };
 
+// Raw exchange: pass A stores the column outputs without the four-step twiddle
+// and pass B applies it from per-thread constants (tensor memory).  Only the
+// kernel pair that implements it: TMA-fed pass A (block transforms) feeding
+// the CP pipeline pass B.  TTAGG_RAWX=0 restores the twiddle in pass A.
+bool raw_exchange(const ttagg_kernel* k) {
+  static const int on = [] {
+    const char* e = getenv("TTAGG_RAWX");
+    return e ? atoi(e) : 1;
+  }();
+  const Geom& g = k->g;
+  return on && k->kind == TTAGG_KIND_CP && g.N2 == 256 && g.N1 >= 1024 && passA_mode() == 1 && passB_tma() &&
+         passB_pipe();
+}
+
 // Pass A (column transforms + loss column sums) and qcoef of one order.
 int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const double* kv, double alpha, bool wantP,
               bool wantQ, ttagg_ctx::Work& w, cudaStream_t st) {
@@ -2066,6 +2154,7 @@ int run_passA(ttagg_ctx* ctx, const ttagg_kernel* k, const double* nv, const dou
   a.nblk = k->nblk;
   a.want_T = wantP ? 1 : 0;
   a.pair0 = 0;
+  a.raw = raw_exchange(k) ? 1 : 0;
   for (int j = 0; j < MAXRES; ++j) {
     a.res_base[j] = P->res_base[j];
     a.res_cnt[j] = P->res_cnt[j];
@@ -2121,6 +2210,7 @@ int run_passBC(ttagg_ctx* ctx, const ttagg_kernel* k, double* p_out, ttagg_ctx::
   for (int i = 0; i <= MAXD; ++i) b.ranks[i] = k->ranks[i];
   b.fdesc = k->fdesc;
   b.pmap = k->pmap;
+  b.raw = raw_exchange(k) ? 1 : 0;
   const int rows = rowsB(g.N2);
   b.nrb = (P->K_rows + rows - 1) / rows;
   b.p0 = 0;

@@ -118,7 +118,8 @@ void run_res(double2* out, double2* tw) {
 
 // The same loop on the [16,16,16] block as pass A uses it today: 256 threads,
 // two CTAs per SM, z in shared memory, split exchanges.
-template <bool TM>
+__constant__ double2 cK[8][16];
+template <bool TM, bool CK = false>
 __global__ void __launch_bounds__(256, 2) bench_res_old(double2* out, const double2* tw, int iters) {
   extern __shared__ __align__(16) double2 sm2[];
   const int t = threadIdx.x;
@@ -153,7 +154,10 @@ __global__ void __launch_bounds__(256, 2) bench_res_old(double2* out, const doub
   for (int it = 0; it < iters; ++it) {
     cplx v[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = cmul(lds_c(zs + t + 256 * r), cmul(tb, lds_c(Kst + r)));
+    for (int r = 0; r < 16; ++r) {
+      const double2 kc = CK ? cK[it % 5][r] : Kst[r];
+      v[r] = cmul(lds_c(zs + t + 256 * r), cmul(tb, mk(kc.x, kc.y)));
+    }
     fft_fwd_split<4096>(v, t, ex, tw, CtaSync(), nullptr, tmw);
     double2* oo = o + (it & 1) * 4096;
 #pragma unroll
@@ -165,21 +169,21 @@ __global__ void __launch_bounds__(256, 2) bench_res_old(double2* out, const doub
     if ((t >> 5) == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm_base) : "memory");
   }
 }
-template <bool TM>
+template <bool TM, bool CK = false>
 void run_res_old(double2* out, double2* tw, int per_sm) {
   const size_t smem = per_sm == 1 ? 120 * 1024 : 65536 + (fft_smem_elems(4096) + 1) * 8;
-  cudaFuncSetAttribute(bench_res_old<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(bench_res_old<TM, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bench_res_old<TM>, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bench_res_old<TM, CK>, 256, smem);
   const int grid = 148 * per_sm, iters = 400;
-  bench_res_old<TM><<<grid, 256, smem>>>(out, tw, 2);
+  bench_res_old<TM, CK><<<grid, 256, smem>>>(out, tw, 2);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   cudaEventRecord(a);
-  bench_res_old<TM><<<grid, 256, smem>>>(out, tw, iters);
+  bench_res_old<TM, CK><<<grid, 256, smem>>>(out, tw, iters);
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
   const double pts = (double)grid * 4096 * iters;
-  printf("res_old tmem_tw=%d 256thr smem=%zu occ=%d/SM: %.3f ms %.2f clk/pt/SM err=%s\n", (int)TM, smem, nb, ms,
+  printf("res_old constK=%d tmem_tw=%d 256thr smem=%zu occ=%d/SM: %.3f ms %.2f clk/pt/SM err=%s\n", (int)CK, (int)TM, smem, nb, ms,
          148 * 1.965e9 * (ms * 1e-3) / pts, cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -208,6 +212,7 @@ int main() {
   std::vector<double2> h(4096), x(4096), r1(4096), r2(4096);
   for (int m = 0; m < 4096; ++m) h[m] = make_double2(cos(2 * M_PI * m / 4096), -sin(2 * M_PI * m / 4096));
   cudaMemcpy(tw, h.data(), 4096 * 16, cudaMemcpyHostToDevice);
+  cudaMemcpyToSymbol(cK, h.data(), sizeof(double2) * 8 * 16);
   unsigned s = 12345;
   for (int m = 0; m < 4096; ++m) {
     s = s * 1664525u + 1013904223u; double a = (s >> 8) / 16777216.0 - 0.5;
@@ -256,10 +261,10 @@ int main() {
   run_wide<2>(out, tw);
   run_wide<3>(out, tw);
   run_wide<4>(out, tw);
-  run_res_old<false>(out, tw, 2);
   run_res_old<true>(out, tw, 2);
-  run_res_old<false>(out, tw, 2);
+  run_res_old<true, true>(out, tw, 2);
   run_res_old<true>(out, tw, 2);
+  run_res_old<true, true>(out, tw, 2);
   run_res_old<false>(out, tw, 1);
   run_res_old<true>(out, tw, 1);
   run_res<2>(out, tw);
