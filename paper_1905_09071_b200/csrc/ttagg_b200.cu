@@ -1067,6 +1067,7 @@ constexpr int PIPE_STG = 8 * 256;                       // one plane of one row 
 constexpr int PIPE_EX = 8 * fft_smem_elems(256);        // row FFT exchange (double2)
 constexpr size_t PIPE_SMEM = (size_t)(2 * PIPE_STG + PIPE_EX) * sizeof(double2);
 
+template <bool RAW>
 __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, const __grid_constant__ CUtensorMap tmT) {
   constexpr int N2 = 256, E = 16, T = 16, SE = fft_smem_elems(N2), ROWS = 8;
   extern __shared__ __align__(128) double2 smem[];
@@ -1112,7 +1113,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
     const int rho = rb * ROWS + rloc;
     const bool valid = rho < a.K_rows;
     const int kap = valid ? max(a.rowkappa[rho], 0) : 0;
-    if (a.raw) {
+    if constexpr (RAW) {
       // the row's four-step twiddles are the same for every pair: built once
       // per row block, parked in tensor memory (16 complex = 64 columns)
 #pragma unroll
@@ -1138,13 +1139,13 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
       // (two 4-value chunks in flight) while the pair's planes are still landing,
       // and multiply the values as they leave the staging regions
       uint32_t fs[2][16];
-      if (a.raw) {
+      if constexpr (RAW) {
         tmem_ld16(tfs, fs[0]);
         tmem_ld16(tfs + 16, fs[1]);
       }
       mbar_wait(&mbar, parity);
       parity ^= 1;
-      if (a.raw) {
+      if constexpr (RAW) {
 #pragma unroll
         for (int q = 0; q < E / 4; ++q) {
           if (q == 0 || q == 2) tmem_wait_ld();
@@ -1156,10 +1157,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
             vp[i] = cmul(lds_c(stP + i * 128 + tid), w);
             vm[i] = cmul(lds_c(stM + i * 128 + tid), w);
           }
-          if (q == 1) {
-            tmem_ld16(tfs + 32, fs[0]);
-            tmem_ld16(tfs + 48, fs[1]);
-          }
+          if (q < 2) tmem_ld16(tfs + 32 + 16 * q, fs[q]);  // chunk q + 2 follows into the buffer just used
         }
       } else {
 #pragma unroll
@@ -1965,8 +1963,9 @@ int launchB(const PassBArgs& a, const CUtensorMap* tm, int grid, cudaStream_t st
   const size_t smem = smemB<N2>();
   if constexpr (N2 == 256) {
     if (tm && !TT && passB_pipe()) {
-      TRY(set_smem(passB_pipe_kernel, PIPE_SMEM));
-      passB_pipe_kernel<<<grid, 128, PIPE_SMEM, st>>>(a, *tm);
+      auto kern = a.raw ? passB_pipe_kernel<true> : passB_pipe_kernel<false>;
+      TRY(set_smem(kern, PIPE_SMEM));
+      kern<<<grid, 128, PIPE_SMEM, st>>>(a, *tm);
       CUDA_TRY(cudaGetLastError());
       return TTAGG_OK;
     }
