@@ -790,9 +790,14 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
   __shared__ __align__(8) uint64_t mbar;  // TMA: both planes of the next pair landed
   __shared__ uint32_t tm_base;            // TT: the second chain accumulator (64 TMEM columns)
   unsigned parity = 0;
-  if constexpr (TT) {
+  // tensor memory: the TT chain's second accumulator (columns 0..63) and, with
+  // a raw exchange (TMA kernels), the row's four-step twiddles (columns 64..127)
+  constexpr bool TMEM = TT || TMA;
+  constexpr unsigned TCOLS = TMA ? 128u : 64u;
+  if constexpr (TMEM) {
     if ((threadIdx.x >> 5) == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&tm_base))
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tm_base)),
+                   "n"(TCOLS)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -818,7 +823,8 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
   const int C = a.C;
   // TT: per-CTA chain scratch (reused by every row block of this CTA)
   const size_t slot = (size_t)blockIdx.x * 2 * a.Rmax;
-  const uint32_t tacc = TT ? tm_base + ((uint32_t)(32 * (tid >> 5)) << 16) : 0u;
+  const uint32_t tacc = TMEM ? tm_base + ((uint32_t)(32 * (tid >> 5)) << 16) : 0u;
+  const uint32_t tfs = tacc + 64;
   auto st = [&](int b, int r, int i) -> double2* {
     return a.scratch + ((slot + (size_t)b * a.Rmax + r) * E + i) * blockDim.x + tid;
   };
@@ -854,6 +860,25 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
     // CP: running product over the modes of one rank term.  TT: chain
     // accumulator of the current state (core, rn); the last group processed
     // is the last core's, so after the loop it holds the chain result.
+    if constexpr (TMA) {
+      if (a.raw) {  // this row's four-step twiddles W_L^(n2 kappa), n2 = t + T i (as passB_pipe_kernel)
+        const int kap0 = valid ? max(a.rowkappa[rho], 0) : 0;
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q) {
+          uint32_t r[16];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const cplx w = twL(a.tabLlo, a.tabLhi, (long long)(t + T * (4 * q + u)) * kap0);
+            r[4 * u + 0] = (uint32_t)__double2loint(w.x);
+            r[4 * u + 1] = (uint32_t)__double2hiint(w.x);
+            r[4 * u + 2] = (uint32_t)__double2loint(w.y);
+            r[4 * u + 3] = (uint32_t)__double2hiint(w.y);
+          }
+          tmem_st16(tfs + 16 * q, r);
+        }
+        tmem_wait_st();
+      }
+    }
     cplx acc[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) acc[i] = mk(0.0, 0.0);
@@ -953,10 +978,32 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
         } else {
           cp_async_wait<0>();
         }
+        bool twiddled = false;
+        if constexpr (TMA) {
+          if (a.raw) {
+            twiddled = true;
 #pragma unroll
-        for (int i = 0; i < E; ++i) {
-          vp[i] = lds_c(stP + i * 128 + tid);
-          vm[i] = lds_c(stM + i * 128 + tid);
+            for (int q = 0; q < E / 4; ++q) {
+              uint32_t r[16];
+              tmem_ld16(tfs + 16 * q, r);
+              tmem_wait_ld();
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = 4 * q + u;
+                const cplx w = mk(__hiloint2double((int)r[4 * u + 1], (int)r[4 * u]),
+                                  __hiloint2double((int)r[4 * u + 3], (int)r[4 * u + 2]));
+                vp[i] = cmul(lds_c(stP + i * 128 + tid), w);
+                vm[i] = cmul(lds_c(stM + i * 128 + tid), w);
+              }
+            }
+          }
+        }
+        if (!twiddled) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            vp[i] = lds_c(stP + i * 128 + tid);
+            vm[i] = lds_c(stM + i * 128 + tid);
+          }
         }
         if constexpr (TT) {
           const int f = __ldg(a.fdesc + 2 * p);
@@ -1043,11 +1090,11 @@ __global__ void __launch_bounds__(128) passB_kernel(const PassBArgs a, const __g
       }
     }
   }
-  if constexpr (TT) {
+  if constexpr (TMEM) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if ((threadIdx.x >> 5) == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tm_base) : "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base), "n"(TCOLS) : "memory");
   }
 }
 
@@ -2104,16 +2151,16 @@ struct ProfScope {
 
 // Raw exchange: pass A stores the column outputs without the four-step twiddle
 // and pass B applies it from per-thread constants (tensor memory).  Only the
-// kernel pair that implements it: TMA-fed pass A (block transforms) feeding
-// the CP pipeline pass B.  TTAGG_RAWX=0 restores the twiddle in pass A.
+// kernels that implement it: the TMA-fed pass A (block transforms) feeding a
+// TMA-fed pass B (N2 = 256; CP pipeline kernel, CP/TT passB_kernel).
+// TTAGG_RAWX=0 restores the twiddle in pass A.
 bool raw_exchange(const ttagg_kernel* k) {
   static const int on = [] {
     const char* e = getenv("TTAGG_RAWX");
     return e ? atoi(e) : 1;
   }();
   const Geom& g = k->g;
-  return on && k->kind == TTAGG_KIND_CP && g.N2 == 256 && g.N1 >= 1024 && passA_mode() == 1 && passB_tma() &&
-         passB_pipe();
+  return on && k->kind != TTAGG_KIND_DENSE && g.N2 == 256 && g.N1 >= 1024 && passA_mode() == 1 && passB_tma();
 }
 
 // Pass A (column transforms + loss column sums) and qcoef of one order.
