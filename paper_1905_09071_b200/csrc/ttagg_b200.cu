@@ -1114,6 +1114,11 @@ constexpr int PIPE_STG = 8 * 256;                       // one plane of one row 
 constexpr int PIPE_EX = 8 * fft_smem_elems(256);        // row FFT exchange (double2)
 constexpr size_t PIPE_SMEM = (size_t)(2 * PIPE_STG + PIPE_EX) * sizeof(double2);
 
+#ifndef TTAGG_B_TMEMTW
+#define TTAGG_B_TMEMTW 1
+#endif
+constexpr unsigned PIPE_TCOLS = TTAGG_B_TMEMTW ? 256u : 128u;
+
 template <bool RAW>
 __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, const __grid_constant__ CUtensorMap tmT) {
   constexpr int N2 = 256, E = 16, T = 16, SE = fft_smem_elems(N2), ROWS = 8;
@@ -1121,7 +1126,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tm_base;
   if ((threadIdx.x >> 5) == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tm_base))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tm_base)), "n"(PIPE_TCOLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -1139,6 +1144,9 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
   double2* ex = smem + 2 * PIPE_STG + rloc * SE;
   const uint32_t tsum = tm_base + ((uint32_t)(32 * (tid >> 5)) << 16);
   const uint32_t tfs = tsum + 64;  // raw exchange: this thread's four-step twiddles W_L^(n2 kappa), n2 = t + 16 i
+  // the row transforms' stage twiddles W_256^(t i) (per thread, as in pass A)
+  const uint32_t tmw = TTAGG_B_TMEMTW ? tsum + 128 : TMW_NONE;
+  if (TTAGG_B_TMEMTW) tmem_store_twiddles16(tmw, a.tw, t * (TW_BASE / 256));
   const int d = a.d, C = a.C;
   unsigned parity = 0;
   auto fetch = [&](int rb, int p) {  // one thread: both planes of pair p of row block rb
@@ -1219,8 +1227,8 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
         if (p + 1 < a.p1) fetch(rb, p + 1);
         else if (nrb < a.nrb) fetch(nrb, a.p0);
       }
-      fft_fwd<N2>(vp, t, ex, a.tw);
-      fft_fwd<N2>(vm, t, ex, a.tw);
+      fft_fwd<N2>(vp, t, ex, a.tw, CtaSync(), nullptr, tmw);
+      fft_fwd<N2>(vm, t, ex, a.tw, CtaSync(), nullptr, tmw);
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const cplx P = vp[i];
@@ -1288,7 +1296,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
       const long long m = ((long long)(d - 1) * k) % a.L;
       S[i] = cmul(S[i], twL(a.tabLlo, a.tabLhi, m));
     }
-    fft_inv<N2>(S, t, ex, a.tw);
+    fft_inv<N2>(S, t, ex, a.tw, CtaSync(), tmw);
     const double wgt = (kap == 0 || 2 * kap == a.K) ? 1.0 : 2.0;
     if (valid) {
 #pragma unroll
@@ -1302,7 +1310,7 @@ __global__ void __launch_bounds__(128, 2) passB_pipe_kernel(const PassBArgs a, c
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if ((threadIdx.x >> 5) == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_base) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base), "n"(PIPE_TCOLS) : "memory");
 }
 
 // ---------------------------------------------------------------------------
