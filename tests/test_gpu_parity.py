@@ -315,7 +315,6 @@ def test_tt_rank_shards_sum_to_full_rhs():
     partial RHS of every slice, each its own upload, sum to the unsharded RHS."""
     import torch
 
-    from paper_1905_09071_b200.construct import tt_rank_shard
 
     N = 5000
     rng = np.random.default_rng(21)
@@ -415,3 +414,45 @@ def test_acceptance_criterion_2_small_sizes(order, n_classes):
         assert rel_inf(g.rhs_cp_Q(kc, st(n)), orc.dense_loss(dc, n)) <= TOL
         assert rel_inf(g.rhs_tt_P(kt, st(n)), orc.dense_gain(dt, n)) <= TOL
         assert rel_inf(g.rhs_tt_Q(kt, st(n)), orc.dense_loss(dt, n)) <= TOL
+
+
+_SWITCH_SCRIPT = r"""
+import sys, numpy as np
+import paper_1905_09071_b200 as g
+from paper_1905_09071_b200.workloads import CONFIGS, initial_state
+N = 1 << 18
+cfg = CONFIGS["C3"]
+fac = cfg.cp_factors(N)
+rng = np.random.default_rng(5)
+tt = g.TTKernel((rng.random((1, N, 3)), rng.random((3, N, 2)), rng.random((2, N, 1))))
+ks = g.KernelSet({2: g.CPKernel(fac[2]), 3: tt, 4: g.CPKernel(fac[4])})
+n = initial_state("exp256", N)
+r = g.rhs_total(ks, g.ConcentrationState(n))
+np.save(sys.argv[1], np.stack([r.p, r.q, r.s]))
+"""
+
+
+@pytest.mark.parametrize("switch", ["TTAGG_RAWX=0", "TTAGG_PASSB_PIPE=0", "TTAGG_PASSA=0", "TTAGG_PASSB_TMA=0"])
+def test_kernel_route_switches_agree(switch, tmp_path):
+    """The A/B switches select other kernels for the same arithmetic (raw
+    exchange off; non-pipeline CP pass B; one-CTA-per-item pass A; cp.async
+    pass B): a CP + TT set at N = 2^18 through each of them (own process — the
+    switches are read once) matches the default route to roundoff."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(extra_env, out):
+        env = dict(os.environ, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        env.update(extra_env)
+        subprocess.run([sys.executable, "-c", _SWITCH_SCRIPT, str(out)], check=True, env=env, cwd=root, timeout=600)
+        return np.load(out)
+
+    ref_path = tmp_path.parent / "route_default.npy"
+    ref = np.load(ref_path) if ref_path.exists() else run({}, ref_path)
+    key, val = switch.split("=")
+    got = run({key: val}, tmp_path / "route.npy")
+    for i, name in enumerate("pqs"):
+        assert rel_inf(got[i], ref[i]) < 1e-12, f"{switch}: {name}"
