@@ -501,11 +501,82 @@ __device__ __forceinline__ void fft_stage_table(double2* stw, const double2* __r
   }
 }
 
+// Length-4096 transform (16 values per thread, 256 threads), split exchanges,
+// tensor-memory stage twiddles with the first half of each stage's twiddles
+// (w^1..w^7) requested before the exchange's last round, so their latency
+// hides behind that round's loads and barrier; the second half is requested
+// while the first is being applied.
+#ifndef TTAGG_TW_HALFPRE
+#define TTAGG_TW_HALFPRE 1
+#endif
+__device__ __forceinline__ cplx tw_slot(const uint32_t (&r)[16], int u) {
+  return mk(__hiloint2double((int)r[4 * u + 1], (int)r[4 * u]), __hiloint2double((int)r[4 * u + 3], (int)r[4 * u + 2]));
+}
+template <class Sync>
+__device__ __forceinline__ void split_exchange16_pre(cplx (&v)[16], const int (&dst)[16], int t, double* sm,
+                                                     const Sync& sync, uint32_t tnext, uint32_t (&w0)[16],
+                                                     uint32_t (&w1)[16]) {
+  constexpr int T = 256;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sm[dst[r]] = v[r].x;
+  sync();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r].x = sm[pad16(t + T * r)];
+  sync();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sm[dst[r]] = v[r].y;
+  sync();
+  tmem_ld16(tnext, w0);
+  tmem_ld16(tnext + 16, w1);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r].y = sm[pad16(t + T * r)];
+  sync();
+}
+__device__ __forceinline__ void tw_apply_halves(cplx (&v)[16], uint32_t taddr, uint32_t (&w0)[16], uint32_t (&w1)[16]) {
+  tmem_wait_ld();
+#pragma unroll
+  for (int u = 1; u < 4; ++u) v[u] = cmul(v[u], tw_slot(w0, u));
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[4 + u] = cmul(v[4 + u], tw_slot(w1, u));
+  tmem_ld16(taddr + 32, w0);
+  tmem_ld16(taddr + 48, w1);
+  tmem_wait_ld();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[8 + u] = cmul(v[8 + u], tw_slot(w0, u));
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[12 + u] = cmul(v[12 + u], tw_slot(w1, u));
+}
+template <class Sync>
+__device__ __forceinline__ void fft4096_split_tm(cplx (&v)[16], int t, double* sm, const Sync& sync, uint32_t tmw) {
+  uint32_t w0[16], w1[16];
+  int dst[16];
+  DFT<16>::run(v);  // stage 1: NS = 1, no twiddles; output i of butterfly q = t goes to 16 q + i
+#pragma unroll
+  for (int i = 0; i < 16; ++i) dst[i] = pad16(t * 16 + i);
+  split_exchange16_pre(v, dst, t, sm, sync, tmw, w0, w1);
+  tw_apply_halves(v, tmw, w0, w1);  // stage 2: NS = 16
+  DFT<16>::run(v);
+  {
+    const int base = (t / 16) * 256 + (t & 15);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dst[i] = pad16(base + i * 16);
+  }
+  split_exchange16_pre(v, dst, t, sm, sync, tmw + 64, w0, w1);
+  tw_apply_halves(v, tmw + 64, w0, w1);  // stage 3: NS = 256 (last): natural order in the registers
+  DFT<16>::run(v);
+}
+
 template <int M, class Sync = CtaSync>
 __device__ __forceinline__ void fft_fwd_split(cplx (&v)[fft_e(M)], int t, double* sm, const double2* __restrict__ tw,
                                               const Sync& sync = Sync(), const double2* stw = nullptr,
                                               uint32_t tmw = TMW_NONE) {
   static_assert(M >= 256 && M <= 4096, "block transforms");
+  if constexpr (M == 4096 && TTAGG_TW_HALFPRE) {
+    if (tmw != TMW_NONE) {
+      fft4096_split_tm(v, t, sm, sync, tmw);
+      return;
+    }
+  }
   constexpr int b = fft_first_radix(M);
   constexpr int a = (ilog2c(M) - ilog2c(b)) / 4;
   constexpr int off = 2 * fft_stage_ns<M>(0);

@@ -275,6 +275,9 @@ struct PMOut {
   cplx cn2;     // W_L^(n2 K) = W_N2^(n2)
 };
 
+#ifndef TTAGG_A_TBPRE
+#define TTAGG_A_TBPRE 1
+#endif
 #ifndef TTAGG_A_TMEMTW
 #define TTAGG_A_TMEMTW 1
 #endif
@@ -700,9 +703,17 @@ __global__ void __launch_bounds__(fft_t(N1), passA_min_ctas(N1)) passA_tma_kerne
     fft_fwd_split<N1>(z, t, ex, a.tw, CtaSync(), stw, tmw);
     if constexpr (RAW) emit_raw<N1>(rbase, o, d, 0, t, z);
     else emit_split<N1>(rbase, o, d, 0, t, z, ct, Pst[pb], PMst[pb]);
+#if TTAGG_A_TBPRE
+    cplx tbn = ld_c(a.tabK + t);  // residue 1's per-thread twist, requested a transform ahead
+#endif
     for (int j = 1; j < d; ++j) {
       cplx v[E];
+#if TTAGG_A_TBPRE
+      const cplx tb = tbn;
+      if (j + 1 < d) tbn = ld_c(a.tabK + (j + 1) * t);
+#else
       const cplx tb = ld_c(a.tabK + j * t);
+#endif
 #pragma unroll
       for (int r = 0; r < E; ++r) v[r] = cmul(lds_c(zs + t + T * r), cmul(tb, lds_c(&Kst[j][r])));
       if (j == d - 1) {

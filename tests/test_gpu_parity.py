@@ -315,6 +315,7 @@ def test_tt_rank_shards_sum_to_full_rhs():
     partial RHS of every slice, each its own upload, sum to the unsharded RHS."""
     import torch
 
+    from paper_1905_09071_b200.construct import tt_rank_shard
 
     N = 5000
     rng = np.random.default_rng(21)
