@@ -327,6 +327,14 @@ __device__ __forceinline__ void emit_split(const int* rbase, const PMOut& o, int
   }
 }
 
+#ifndef TTAGG_EMIT_CS
+#define TTAGG_EMIT_CS 1
+#endif
+#if TTAGG_EMIT_CS
+#define EMIT_ST stg_cs
+#else
+#define EMIT_ST sts_c
+#endif
 // emit_split for a raw exchange (raw_exchange()): the four-step twiddle
 // W_L^(n2 kappa) is the same for the P row kappa and the M row kappa (see
 // emit_pm), depends on (row, n2) only and not on the column pair, so pass B
@@ -336,13 +344,13 @@ __device__ __forceinline__ void emit_raw(const int* rbase, const PMOut& o, int d
   constexpr int T = N1 / 16;
   double2* TP = o.TP + rbase[j];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) sts_c(TP + t + T * r, v[r]);
+  for (int r = 0; r < 8; ++r) EMIT_ST(TP + t + T * r, v[r]);
   double2* TM = j == 0 ? o.TM + rbase[0] + N1 - t : o.TM + rbase[d - j] + (N1 - 1 - t);
 #pragma unroll
-  for (int r = 8; r < 16; ++r) sts_c(TM - T * r, cconj(v[r]));
+  for (int r = 8; r < 16; ++r) EMIT_ST(TM - T * r, cconj(v[r]));
   if (t == 0 && j == 0) {
-    sts_c(o.TM + rbase[0], cconj(v[0]));
-    sts_c(TP + T * 8, v[8]);
+    EMIT_ST(o.TM + rbase[0], cconj(v[0]));
+    EMIT_ST(TP + T * 8, v[8]);
   }
 }
 
