@@ -526,11 +526,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
 }
 // 1-D bulk copy global -> shared (TMA engine), completion counted on mbarrier m
+#ifndef TTAGG_L2_HINT
+#define TTAGG_L2_HINT 1
+#endif
+// L2 policy for data read exactly once per RHS (pass A's factor-column rows: -0.03 ms on A5; the same hint on
+// pass B's exchange reads measured +0.05 ms and is not used)
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
+#if TTAGG_L2_HINT
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(m)), "l"(l2_evict_first())
+      : "memory");
+#else
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(m))
                : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
   asm volatile(
