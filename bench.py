@@ -326,8 +326,13 @@ def extras(ctx, dev, stream, peak, steps):
     # D = 4 at N = 2^20 (orders 2..4, CP ranks 2/6/24, the C5 exponents / state)
     ks, dks, B = cp_set(c5.exponents, (2, 3, 4), N)
     ms = _timed_rhs(ctx, dks, initial_state("c5", N), dev, stream, steps)
-    out["d4_n2p20"] = {"rhs_per_s": 1e3 / ms, "ms_per_rhs": ms, "model_frac": frac(B, ms),
-                       "workload": "D=4 (d=2..4), N=2^20, CP ranks 2/6/24 (C5 exponents and state)"}
+    # RK2 at the same size (mass-normalised state, the C5 step size; 20 steps)
+    r4 = _rk2_rate(ctx, dks, initial_state("c5", N, normalised=True), c5.dt, 20)
+    r4["model_frac_marginal"] = (frac(2 * B, 1e3 / r4["steps_per_s_marginal"])
+                                 if r4["steps_per_s_marginal"] else None)
+    out["d4_n2p20"] = {"rhs_per_s": 1e3 / ms, "ms_per_rhs": ms, "model_frac": frac(B, ms), "rk2": r4,
+                       "workload": "D=4 (d=2..4), N=2^20, CP ranks 2/6/24 (C5 exponents and state); "
+                                   "RK2 dt=0.002, 20 steps (normalised state)"}
     del ks, dks
     # C2: 1000 back-to-back RHS calls at N = 65536, D = 3
     c2 = CONFIGS["C2"]
